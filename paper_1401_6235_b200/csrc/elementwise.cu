@@ -1,0 +1,284 @@
+// elementwise.cu — the 22 twofold kernels (+ the two raw exact-transform loops)
+// over split (value, error) planes, f32 and f64.
+//
+// Replaces the reference loop drivers _loop22/_loop21/_loop11/_loop1u
+// (kernels.py:79-113): out[i] = core(in[i]) for every i, each output index
+// written exactly once.  HBM-bound: per element the kernel moves
+// (NIN + 2) * sizeof(T) bytes and nothing else.
+//
+// Layout in HBM: each plane is one contiguous 1-D array (SoA, kernels.py:3-5).
+// Design: a persistent grid (resident CTAs only, sized by the occupancy
+// calculator for 148 SMs) grid-strides over 16-byte vectors; each thread
+// issues UNROLL x NIN independent 128-bit streaming loads before any math, so
+// every SM keeps >= 64 KB of reads in flight.  Planes that share a common
+// misalignment get a scalar head; the n % (16/sizeof(T)) tail is scalar too —
+// both handled by the same launch.  Planes with different misalignments run
+// the scalar grid-stride path (still one launch).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "tf_math.cuh"
+
+namespace tf {
+
+template <class T>
+struct Planes {
+  const T* in[4];
+  T* out[2];
+};
+
+template <int NIN>
+struct Unroll {
+  static constexpr int U = NIN >= 4 ? 2 : (NIN == 3 ? 2 : 4);
+};
+
+template <class T, int OP>
+__device__ __forceinline__ void scalar_elem(const Planes<T>& p, int64_t i) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  T v[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; k++) v[k] = ld_stream(p.in[k] + i);
+  P<T> z = apply<T, OP>(v);
+  st_stream(p.out[0] + i, z.a);
+  st_stream(p.out[1] + i, z.b);
+}
+
+template <class T, int OP>
+__global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t head,
+                                                 int64_t nvec) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  constexpr int E = Vec16<T>::N;
+  constexpr int U = Unroll<NIN>::U;
+  using V = typename Vec16<T>::type;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+
+  // scalar head (common misalignment) — or everything, when nvec == 0
+  for (int64_t i = gtid; i < head; i += gstride) scalar_elem<T, OP>(p, i);
+  // scalar tail
+  const int64_t tail0 = head + nvec * E;
+  for (int64_t i = tail0 + gtid; i < n; i += gstride) scalar_elem<T, OP>(p, i);
+
+  // 16-byte-vector body
+  const V* vin[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; k++) vin[k] = reinterpret_cast<const V*>(p.in[k] + head);
+  V* vo0 = reinterpret_cast<V*>(p.out[0] + head);
+  V* vo1 = reinterpret_cast<V*>(p.out[1] + head);
+
+  for (int64_t base = gtid; base < nvec; base += gstride * U) {
+    V r[U][NIN];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * gstride;
+      if (j < nvec) {
+#pragma unroll
+        for (int k = 0; k < NIN; k++) r[u][k] = ld_stream(vin[k] + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * gstride;
+      if (j < nvec) {
+        V o0, o1;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          T v[NIN];
+#pragma unroll
+          for (int k = 0; k < NIN; k++) v[k] = lane<T>(r[u][k], e);
+          P<T> z = apply<T, OP>(v);
+          set_lane<T>(o0, e, z.a);
+          set_lane<T>(o1, e, z.b);
+        }
+        st_stream(vo0 + j, o0);
+        st_stream(vo1 + j, o1);
+      }
+    }
+  }
+}
+
+// ---- dispatch ------------------------------------------------------------------
+
+using EwFn = void (*)(Planes<double>, int64_t, int64_t, int64_t);
+
+struct EwEntry {
+  const void* fn;  // kernel symbol
+  int nin;
+  int unroll;
+  int max_blocks_per_sm;  // occupancy, filled lazily
+};
+
+template <class T, int OP>
+EwEntry make_entry() {
+  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP>), OpInfo<OP>::NIN,
+                 Unroll<OpInfo<OP>::NIN>::U, 0};
+}
+
+template <class T, int... OPS>
+struct Table {
+  static EwEntry* get() {
+    static EwEntry t[] = {make_entry<T, OPS>()...};
+    return t;
+  }
+};
+
+static EwEntry* table_for(int dtype) {
+  if (dtype == TF_F64)
+    return Table<double, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
+                 21, 22, 23>::get();
+  return Table<float, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
+               22, 23>::get();
+}
+
+int ew_num_inputs(int op) {
+  static const int nin[TF_NUM_OPS] = {4, 4, 4, 4, 3, 3, 3, 3, 2, 2, 2, 2,
+                                      2, 1, 4, 4, 4, 4, 3, 3, 3, 3, 2, 1};
+  if (op < 0 || op >= TF_NUM_OPS) return TF_EINVAL;
+  return nin[op];
+}
+
+int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* out,
+              cudaStream_t stream) {
+  if (op < 0 || op >= TF_NUM_OPS) return fail(TF_EINVAL, "tf_elementwise: unknown op id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, "tf_elementwise: planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, "tf_elementwise: negative length");
+  if (n == 0) return TF_OK;
+  EwEntry& ent = table_for(dtype)[op];
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  const int E = (int)(16 / tsz);
+  if (!in || !out || !out[0] || !out[1]) return fail(TF_EINVAL, "tf_elementwise: null plane");
+  for (int k = 0; k < ent.nin; k++)
+    if (!in[k]) return fail(TF_EINVAL, "tf_elementwise: null plane");
+
+  // common misalignment -> scalar head, else all-scalar
+  uintptr_t mis = reinterpret_cast<uintptr_t>(out[0]) & 15u;
+  bool same = (mis % tsz) == 0 && (reinterpret_cast<uintptr_t>(out[1]) & 15u) == mis;
+  for (int k = 0; k < ent.nin; k++) same = same && (reinterpret_cast<uintptr_t>(in[k]) & 15u) == mis;
+  int64_t head, nvec;
+  if (same) {
+    head = mis ? (int64_t)((16 - mis) / tsz) : 0;
+    if (head > n) head = n;
+    nvec = (n - head) / E;
+  } else {
+    head = n;
+    nvec = 0;
+  }
+
+  if (ent.max_blocks_per_sm == 0) {
+    int b = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ent.fn, 256, 0);
+    if (e != cudaSuccess) return cuda_status(e, "tf_elementwise: occupancy");
+    ent.max_blocks_per_sm = b > 0 ? b : 1;
+  }
+  const int64_t work = nvec > 0 ? (nvec + ent.unroll - 1) / ent.unroll : n;
+  int64_t blocks = (work + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * ent.max_blocks_per_sm;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+
+  Planes<double> p{};  // bit-identical layout for float: only pointers
+  for (int k = 0; k < ent.nin; k++) p.in[k] = static_cast<const double*>(in[k]);
+  p.out[0] = static_cast<double*>(out[0]);
+  p.out[1] = static_cast<double*>(out[1]);
+  void* args[] = {&p, &n, &head, &nvec};
+  cudaError_t e = cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, stream);
+  return cuda_status(e, "tf_elementwise: launch");
+}
+
+// ---- dotted baselines + copy (bench.py:56-87) --------------------------------
+
+template <class T, int BASE>
+__global__ void __launch_bounds__(256) dotted_kernel(const T* __restrict__ x,
+                                                     const T* __restrict__ y, T* __restrict__ r,
+                                                     int64_t n) {
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = gtid; i < n; i += gstride) {
+    T a = ld_stream(x + i), v;
+    if constexpr (BASE == 0) v = add(a, ld_stream(y + i));
+    else if constexpr (BASE == 1) v = mul(a, ld_stream(y + i));
+    else if constexpr (BASE == 2) v = dvd(a, ld_stream(y + i));
+    else if constexpr (BASE == 3) v = sqr(a);
+    else v = a;
+    st_stream(r + i, v);
+  }
+}
+
+template <class T, int BASE>
+__global__ void __launch_bounds__(256) dotted_vec_kernel(const typename Vec16<T>::type* __restrict__ x,
+                                                         const typename Vec16<T>::type* __restrict__ y,
+                                                         typename Vec16<T>::type* __restrict__ r,
+                                                         int64_t nvec) {
+  using V = typename Vec16<T>::type;
+  constexpr int E = Vec16<T>::N;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = gtid; base < nvec; base += 4 * gstride) {
+    V a[4], b[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      int64_t j = base + u * gstride;
+      if (j < nvec) {
+        a[u] = ld_stream(x + j);
+        if constexpr (BASE <= 2) b[u] = ld_stream(y + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      int64_t j = base + u * gstride;
+      if (j < nvec) {
+        V o;
+#pragma unroll
+        for (int e = 0; e < E; e++) {
+          T s = lane<T>(a[u], e), v;
+          if constexpr (BASE == 0) v = add(s, lane<T>(b[u], e));
+          else if constexpr (BASE == 1) v = mul(s, lane<T>(b[u], e));
+          else if constexpr (BASE == 2) v = dvd(s, lane<T>(b[u], e));
+          else if constexpr (BASE == 3) v = sqr(s);
+          else v = s;
+          set_lane<T>(o, e, v);
+        }
+        st_stream(r + j, o);
+      }
+    }
+  }
+}
+
+template <class T, int BASE>
+static int dotted_t(int64_t n, const void* x, const void* y, void* r, cudaStream_t s) {
+  constexpr int E = Vec16<T>::N;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  const bool vec = aligned16(x) && aligned16(r) && (BASE > 2 || aligned16(y)) && n % E == 0;
+  if (vec) {
+    int64_t nvec = n / E;
+    int64_t blocks = (nvec / 4 + 255) / 256;
+    blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
+    dotted_vec_kernel<T, BASE><<<(unsigned)blocks, 256, 0, s>>>(
+        static_cast<const typename Vec16<T>::type*>(x),
+        static_cast<const typename Vec16<T>::type*>(y ? y : x),
+        static_cast<typename Vec16<T>::type*>(r), nvec);
+  } else {
+    int64_t blocks = (n + 255) / 256;
+    blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
+    dotted_kernel<T, BASE><<<(unsigned)blocks, 256, 0, s>>>(
+        static_cast<const T*>(x), static_cast<const T*>(y ? y : x), static_cast<T*>(r), n);
+  }
+  return launch_status("tf_dotted");
+}
+
+int dotted_launch(int base, int dtype, int64_t n, const void* x, const void* y, void* r,
+                  cudaStream_t s) {
+  if (n < 0 || (dtype != TF_F32 && dtype != TF_F64) || base < 0 || base > 4 || !x || !r)
+    return fail(TF_EINVAL, "tf_dotted: bad arguments");
+  if (n == 0) return TF_OK;
+  if (base <= 2 && !y) return fail(TF_EINVAL, "tf_dotted: null y");
+#define D(B)                                                                       \
+  case B:                                                                          \
+    return dtype == TF_F64 ? dotted_t<double, B>(n, x, y, r, s) : dotted_t<float, B>(n, x, y, r, s);
+  switch (base) { D(0) D(1) D(2) D(3) D(4) }
+#undef D
+  return TF_EINVAL;
+}
+
+}  // namespace tf

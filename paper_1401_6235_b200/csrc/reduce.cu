@@ -1,0 +1,334 @@
+// reduce.cu — twofold sum / twofold-input sum / dot in the canonical order, and
+// the cross-shard combine.
+//
+// The reference has no reduction API; its only reduction is the serial
+// _accumulate fold of _tadd (demos.py:107-113).  These kernels compose the same
+// cores (_tadd1, _tadd, _two_prod: arith.py:61-71, fp_core.py:170-173) in a
+// fixed, data-parallel order that the CPU oracle restates exactly:
+//
+//   tile t holds elements [t*L, (t+1)*L), L = V*W*K (V elements per 16-byte
+//   vector, W = 256 lanes, K = 128 vectors per lane);
+//   lane w folds elements t*L + V*(w + W*k) + v, k-major then v, starting from
+//   its first element ((x,+0) | (x0,x1) | TwoProd(x,y));
+//   lanes, then tiles, combine in the adjacent-pair (stride-doubling) _tadd tree,
+//   lower index on the left, absent nodes skipped (never padded).
+//
+// One CTA per tile: 256 threads issue 8 x 16-byte loads each per batch
+// (coalesced: consecutive lanes read consecutive vectors), fold in registers,
+// reduce through warp shuffles and shared memory, and publish a 16-byte tile
+// partial.  The last CTA to finish (atomic ticket, never arrival order for the
+// arithmetic) folds all tile partials with the same tree, so the whole reduction
+// is one launch and bit-deterministic.  HBM-bound: sizeof(T) bytes per element
+// per input plane.
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "tf_math.cuh"
+
+namespace tf {
+
+constexpr int RW = 256;  // lanes per tile
+constexpr int RK = 128;  // vectors per lane
+constexpr int RKB = 8;   // vectors per load batch
+
+template <class T>
+struct Geo {
+  static constexpr int V = Vec16<T>::N;
+  static constexpr int64_t L = (int64_t)V * RW * RK;
+};
+
+// fold one element into a lane accumulator
+template <class T, int ROP>
+__device__ __forceinline__ P<T> first_term(T x, T y) {
+  if constexpr (ROP == TF_RSUM) return {x, T(0)};
+  else if constexpr (ROP == TF_RSUM2) return {x, y};
+  else return two_prod(x, y);
+}
+template <class T, int ROP>
+__device__ __forceinline__ P<T> fold(P<T> acc, T x, T y) {
+  if constexpr (ROP == TF_RSUM) return tadd1(acc.a, acc.b, x);
+  else if constexpr (ROP == TF_RSUM2) return tadd(acc.a, acc.b, x, y);
+  else {
+    P<T> p = two_prod(x, y);
+    return tadd(acc.a, acc.b, p.a, p.b);
+  }
+}
+
+template <class T>
+__device__ __forceinline__ P<T> comb(P<T> l, P<T> r) {
+  return tadd(l.a, l.b, r.a, r.b);
+}
+
+// adjacent-pair tree across the 32 lanes of a warp (absent lanes form a suffix)
+template <class T>
+__device__ __forceinline__ void warp_tree(P<T>& acc, int& have, int lane, int width) {
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    if (off >= width) break;
+    T oa = __shfl_down_sync(0xffffffffu, acc.a, off);
+    T ob = __shfl_down_sync(0xffffffffu, acc.b, off);
+    int oh = __shfl_down_sync(0xffffffffu, have, off);
+    if ((lane & (2 * off - 1)) == 0 && oh && (lane + off) < width) {
+      acc = comb(acc, P<T>{oa, ob});
+    }
+  }
+}
+
+// Sequential evaluation of the skip tree over items [lo, hi) of an aligned block:
+// binary-counter stack, then a right fold of what is left.
+template <class T>
+__device__ __forceinline__ P<T> block_tree(const P<T>* items, int64_t lo, int64_t hi) {
+  P<T> st[40];
+  int lv[40];
+  int sp = 0;
+  for (int64_t i = lo; i < hi; i++) {
+    P<T> v = P<T>{__ldcg(&items[i].a), __ldcg(&items[i].b)};
+    int l = 0;
+    while (sp > 0 && lv[sp - 1] == l) {
+      v = comb(st[sp - 1], v);
+      sp--;
+      l++;
+    }
+    st[sp] = v;
+    lv[sp] = l;
+    sp++;
+  }
+  P<T> acc = st[sp - 1];
+  for (int s = sp - 2; s >= 0; s--) acc = comb(st[s], acc);
+  return acc;
+}
+
+// CTA-wide skip tree over one value per thread (threads with have==0 form a suffix)
+template <class T>
+__device__ __forceinline__ P<T> cta_tree(P<T> acc, int have, int* have_out) {
+  __shared__ T sa[RW / 32], sb[RW / 32];
+  __shared__ int sh[RW / 32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  warp_tree(acc, have, lane, 32);
+  if (lane == 0) {
+    sa[warp] = acc.a;
+    sb[warp] = acc.b;
+    sh[warp] = have;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = RW / 32;
+    P<T> w = lane < nw ? P<T>{sa[lane], sb[lane]} : P<T>{T(0), T(0)};
+    int h = lane < nw ? sh[lane] : 0;
+    warp_tree(w, h, lane, nw);
+    acc = w;
+    have = h;
+  }
+  *have_out = have;
+  return acc;
+}
+
+template <class T, int ROP, bool VEC>
+__global__ void __launch_bounds__(RW) reduce_kernel(const T* __restrict__ a,
+                                                    const T* __restrict__ b, int64_t n,
+                                                    int64_t ntiles, P<T>* tiles,
+                                                    unsigned* counter, T* out) {
+  constexpr int V = Geo<T>::V;
+  constexpr int64_t L = Geo<T>::L;
+  using Vt = typename Vec16<T>::type;
+  const int w = threadIdx.x;
+  const int64_t t = blockIdx.x;
+  const int64_t base = t * L;
+  P<T> acc{T(0), T(0)};
+  int have = 0;
+
+  if (VEC && base + L <= n) {
+    // full tile, 16-byte aligned planes
+    const Vt* va = reinterpret_cast<const Vt*>(a + base) + w;
+    const Vt* vb = reinterpret_cast<const Vt*>((ROP == TF_RSUM ? a : b) + base) + w;
+#pragma unroll 1
+    for (int k0 = 0; k0 < RK; k0 += RKB) {
+      Vt ra[RKB], rb[RKB];
+#pragma unroll
+      for (int kb = 0; kb < RKB; kb++) {
+        ra[kb] = ld_stream(va + (int64_t)RW * (k0 + kb));
+        if constexpr (ROP != TF_RSUM) rb[kb] = ld_stream(vb + (int64_t)RW * (k0 + kb));
+      }
+#pragma unroll
+      for (int kb = 0; kb < RKB; kb++) {
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          T x = lane<T>(ra[kb], e);
+          T y = (ROP == TF_RSUM) ? x : lane<T>(rb[kb], e);
+          if (k0 == 0 && kb == 0 && e == 0) acc = first_term<T, ROP>(x, y);
+          else acc = fold<T, ROP>(acc, x, y);
+        }
+      }
+    }
+    have = 1;
+  } else {
+    // partial tile or unaligned planes: same order, scalar loads, bounds checked
+    for (int k = 0; k < RK; k++) {
+      for (int e = 0; e < V; e++) {
+        const int64_t i = base + (int64_t)V * (w + (int64_t)RW * k) + e;
+        if (i >= n) continue;
+        T x = ld_stream(a + i);
+        T y = (ROP == TF_RSUM) ? x : ld_stream(b + i);
+        if (!have) {
+          acc = first_term<T, ROP>(x, y);
+          have = 1;
+        } else {
+          acc = fold<T, ROP>(acc, x, y);
+        }
+      }
+    }
+  }
+
+  int h;
+  acc = cta_tree(acc, have, &h);
+
+  __shared__ int is_last;
+  if (threadIdx.x == 0) {
+    tiles[t].a = acc.a;
+    tiles[t].b = acc.b;
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    is_last = (prev == (unsigned)(ntiles - 1));
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+
+  // last CTA: the tile tree.  Thread j owns the aligned block of B2 tiles
+  // [j*B2, (j+1)*B2); blocks are complete subtrees, so block trees followed by
+  // the CTA tree reproduce the global adjacent-pair tree exactly.
+  int64_t per = (ntiles + RW - 1) / RW;
+  int64_t B2 = 1;
+  while (B2 < per) B2 <<= 1;
+  const int64_t lo = (int64_t)threadIdx.x * B2;
+  const int64_t hi = lo + B2 < ntiles ? lo + B2 : ntiles;
+  P<T> part{T(0), T(0)};
+  int ph = 0;
+  if (lo < ntiles) {
+    part = block_tree(tiles, lo, hi);
+    ph = 1;
+  }
+  __syncthreads();  // shared scratch of cta_tree is reused
+  part = cta_tree(part, ph, &h);
+  if (threadIdx.x == 0) {
+    out[0] = part.a;
+    out[1] = part.b;
+    *counter = 0u;  // leave the workspace ready for the next call
+  }
+}
+
+struct ShardIdx {
+  short v[1024];  // indices of the non-empty shards, in shard order
+  int m;
+};
+
+template <class T>
+__global__ void combine_kernel(const T* partials, ShardIdx idx, T* out) {
+  // one thread: the skip tree over the m non-empty shards, in shard order
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const int m = idx.m;
+  if (m == 0) {
+    out[0] = T(0);
+    out[1] = T(0);
+    return;
+  }
+  P<T> st[40];
+  int lv[40];
+  int sp = 0;
+  for (int q = 0; q < m; q++) {
+    P<T> v{partials[2 * idx.v[q]], partials[2 * idx.v[q] + 1]};
+    int l = 0;
+    while (sp > 0 && lv[sp - 1] == l) {
+      v = comb(st[sp - 1], v);
+      sp--;
+      l++;
+    }
+    st[sp] = v;
+    lv[sp] = l;
+    sp++;
+  }
+  P<T> acc = st[sp - 1];
+  for (int s = sp - 2; s >= 0; s--) acc = comb(st[s], acc);
+  out[0] = acc.a;
+  out[1] = acc.b;
+}
+
+// ---- host side -------------------------------------------------------------------
+
+static int64_t tiles_for(int dtype, int64_t n) {
+  const int64_t L = dtype == TF_F64 ? Geo<double>::L : Geo<float>::L;
+  return (n + L - 1) / L;
+}
+
+size_t reduce_ws_bytes(int dtype, int64_t n) {
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  return 256 + (size_t)tiles_for(dtype, n) * 2 * tsz;
+}
+
+int reduce_geometry(int dtype, int* V, int* W, int* K) {
+  if (dtype != TF_F32 && dtype != TF_F64) return fail(TF_EINVAL, "tf_reduce_geometry: dtype");
+  if (V) *V = dtype == TF_F64 ? Geo<double>::V : Geo<float>::V;
+  if (W) *W = RW;
+  if (K) *K = RK;
+  return TF_OK;
+}
+
+template <class T, int ROP>
+static int reduce_t(int64_t n, const void* a, const void* b, void* out, void* ws,
+                    cudaStream_t s) {
+  const int64_t nt = tiles_for(sizeof(T) == 8 ? TF_F64 : TF_F32, n);
+  unsigned* counter = static_cast<unsigned*>(ws);
+  P<T>* tiles = reinterpret_cast<P<T>*>(static_cast<char*>(ws) + 256);
+  const bool vec = aligned16(a) && (ROP == TF_RSUM || aligned16(b));
+  const T* pa = static_cast<const T*>(a);
+  const T* pb = static_cast<const T*>(b ? b : a);
+  if (vec)
+    reduce_kernel<T, ROP, true><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
+                                                            static_cast<T*>(out));
+  else
+    reduce_kernel<T, ROP, false><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
+                                                             static_cast<T*>(out));
+  return launch_status("tf_reduce");
+}
+
+int reduce_launch(int rop, int dtype, int64_t n, const void* a, const void* b, void* out,
+                  void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (rop < 0 || rop >= TF_NUM_ROPS) return fail(TF_EINVAL, "tf_reduce: unknown reduction id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, "tf_reduce: planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, "tf_reduce: negative length");
+  if (!out) return fail(TF_EINVAL, "tf_reduce: null output");
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  if (n == 0) return cuda_status(cudaMemsetAsync(out, 0, 2 * tsz, s), "tf_reduce: zero");
+  if (!a || (rop != TF_RSUM && !b)) return fail(TF_EINVAL, "tf_reduce: null plane");
+  if (!ws || ws_bytes < reduce_ws_bytes(dtype, n))
+    return fail(TF_EINVAL, "tf_reduce: workspace too small");
+  if (tiles_for(dtype, n) > 0x7fffffffLL) return fail(TF_EINVAL, "tf_reduce: too many tiles");
+#define R(ROP)                                                            \
+  case ROP:                                                               \
+    return dtype == TF_F64 ? reduce_t<double, ROP>(n, a, b, out, ws, s)   \
+                           : reduce_t<float, ROP>(n, a, b, out, ws, s);
+  switch (rop) { R(TF_RSUM) R(TF_RSUM2) R(TF_RDOT) }
+#undef R
+  return TF_EINVAL;
+}
+
+int combine_launch(int dtype, int g, const void* partials, const int64_t* counts, void* out,
+                   cudaStream_t s) {
+  if (dtype != TF_F32 && dtype != TF_F64) return fail(TF_EINVAL, "tf_combine: dtype");
+  if (g < 0 || g > 1024) return fail(TF_EINVAL, "tf_combine: shard count out of range");
+  if (!out || (g > 0 && (!partials || !counts))) return fail(TF_EINVAL, "tf_combine: null pointer");
+  ShardIdx idx;
+  idx.m = 0;
+  for (int r = 0; r < g; r++)
+    if (counts[r] > 0) idx.v[idx.m++] = (short)r;
+  if (dtype == TF_F64)
+    combine_kernel<double><<<1, 32, 0, s>>>(static_cast<const double*>(partials), idx,
+                                            static_cast<double*>(out));
+  else
+    combine_kernel<float><<<1, 32, 0, s>>>(static_cast<const float*>(partials), idx,
+                                           static_cast<float*>(out));
+  return launch_status("tf_combine");
+}
+
+}  // namespace tf

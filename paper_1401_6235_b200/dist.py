@@ -1,0 +1,112 @@
+"""Multi-GPU sharding: one process per GPU (torch.distributed over NCCL).
+
+Elementwise kernels and Horner shard into independent contiguous slices with no
+communication at all.  Reductions have one real exchange step: every rank
+reduces its shard to a 16-byte twofold partial, the partials are all-gathered
+(NCCL over NVLink/NVSwitch), and every rank folds them with the same
+adjacent-pair ``_tadd`` tree (``tf_combine``).  NCCL's own sum is never used:
+it drops z1 and its order depends on topology.
+
+Shards for reductions are blocks of B = 2^ceil(log2(ceil(T/G))) whole tiles
+(T tiles of L elements, G ranks), so each shard is a complete subtree of the
+canonical tree: the result is bit-identical for every G and to the one-GPU
+result ("Canonical reduction order").
+"""
+
+from __future__ import annotations
+
+from typing import Callable, Optional, Sequence, Tuple
+
+try:
+    import torch
+    import torch.distributed as dist
+except Exception:  # pragma: no cover
+    torch = None
+    dist = None
+
+
+def shard_elementwise(n: int, world: int, rank: int, align: int = 2) -> Tuple[int, int]:
+    """Contiguous [lo, hi) slice of n elements for `rank`, cut at multiples of
+    `align` elements (16-byte boundaries keep every shard on the vector path)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    per = -(-n // world)
+    per = -(-per // align) * align
+    lo = min(rank * per, n)
+    hi = min(lo + per, n)
+    return lo, hi
+
+
+def shard_tiles(n: int, world: int, rank: int, tile: int) -> Tuple[int, int]:
+    """Element range [lo, hi) of `rank`'s reduction shard: an aligned
+    power-of-two block of whole tiles (a complete subtree of the tile tree)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    T = -(-n // tile)
+    per = -(-T // world) if T else 0
+    B = 1
+    while B < per:
+        B <<= 1
+    t0 = min(rank * B, T)
+    t1 = min(t0 + B, T)
+    return min(t0 * tile, n), min(t1 * tile, n)
+
+
+def shard_counts(n: int, world: int, tile: int) -> list:
+    return [hi - lo for lo, hi in (shard_tiles(n, world, r, tile) for r in range(world))]
+
+
+def gather_partials(partial, group=None):
+    """All-gather each rank's 2-element partial into a (world, 2) tensor (rank order)."""
+    world = dist.get_world_size(group)
+    out = torch.empty((world, 2), dtype=partial.dtype, device=partial.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_gather_into_tensor(out, partial.reshape(2).contiguous(), group=group)
+    else:
+        parts = [torch.empty(2, dtype=partial.dtype, device=partial.device) for _ in range(world)]
+        dist.all_gather(parts, partial.reshape(2).contiguous(), group=group)
+        for r in range(world):
+            out[r] = parts[r]
+    return out
+
+
+def sharded_reduce(rop: str, local: Sequence, n: int, group=None,
+                   reduce_fn: Optional[Callable] = None,
+                   combine_fn: Optional[Callable] = None, tile: Optional[int] = None):
+    """Reduce a globally sharded plane set; every rank returns the same Twofold.
+
+    ``local`` holds this rank's planes (its shard_tiles slice).  reduce_fn /
+    combine_fn default to the device kernels; tests on CPU (gloo) inject others.
+    """
+    from . import reduce as R
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    if tile is None:
+        import numpy as np
+
+        dt = np.float64 if local[0].dtype == torch.float64 else np.float32
+        tile = R.tile_elems(dt)
+    lo, hi = shard_tiles(n, world, rank, tile)
+    if local[0].shape[0] != hi - lo:
+        raise ValueError("sharded_reduce: rank %d holds %d elements, its shard is %d"
+                         % (rank, local[0].shape[0], hi - lo))
+    if reduce_fn is None:
+        fn = {"sum": R.vtsum, "sum2": lambda a, b, out: R.vtsum2((a, b), out=out),
+              "dot": R.vtdot}[rop]
+        part = torch.empty(2, dtype=local[0].dtype, device=local[0].device)
+        if hi > lo:
+            fn(*local, out=part)
+        else:
+            part.zero_()
+    else:
+        part = reduce_fn(rop, local)
+    allp = gather_partials(part, group)
+    counts = shard_counts(n, world, tile)
+    if combine_fn is None:
+        return R.combine(allp, counts)
+    return combine_fn(allp, counts)
+
+
+__all__ = ["shard_elementwise", "shard_tiles", "shard_counts", "gather_partials",
+           "sharded_reduce"]

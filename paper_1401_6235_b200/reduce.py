@@ -1,0 +1,159 @@
+"""Twofold reductions (sum, twofold-input sum, dot) and twofold Horner on B200.
+
+The reference has no array API for these (its only reduction is the serial
+``_accumulate`` fold of ``_tadd``, demos.py:107-113).  They are composed from
+the reference cores — ``_tadd1`` (arith.py:67-71), ``_tadd`` (arith.py:61-64),
+``_two_prod`` (fp_core.py:170-173), ``_tmul1`` (arith.py:97-101) — in the
+canonical order documented in DESIGN.md, which the CPU oracle restates, so
+results are bit-exact against it and bit-identical for any number of shards.
+
+    vtsum(x)          -> Twofold   Σ x_i           (z0 = plain sum in that order)
+    vtsum2(x)         -> Twofold   Σ (x0_i + x1_i) for a TwofoldArray x
+    vtdot(x, y)       -> Twofold   Σ x_i * y_i
+    vthorner(c, x, out)            twofold Horner of Σ c_k x^k at every x_i
+
+Reductions return a ``Twofold`` of Python floats (one device->host read of 16
+bytes) unless ``out=`` (a 2-element CUDA tensor) is given, in which case they
+stay asynchronous on the current stream.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections import namedtuple
+
+import numpy as np
+
+from . import _lib
+from .kernels import TwofoldArray, _check, _describe, _dtype_id
+
+try:
+    import torch
+except Exception:  # pragma: no cover
+    torch = None
+
+Twofold = namedtuple("Twofold", ("value", "error"))
+
+_WS = {}  # (device, dtype) -> workspace tensor (zeroed once; the kernel leaves it zeroed)
+
+
+def geometry(dtype=np.float64):
+    """(V, W, K) of the canonical order for a plane dtype."""
+    V, W, K = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    dt = _lib.TF_F64 if np.dtype(dtype) == np.float64 else _lib.TF_F32
+    _lib.check(_lib.lib().tf_reduce_geometry(dt, ctypes.byref(V), ctypes.byref(W),
+                                             ctypes.byref(K)), "geometry")
+    return V.value, W.value, K.value
+
+
+def tile_elems(dtype=np.float64) -> int:
+    V, W, K = geometry(dtype)
+    return V * W * K
+
+
+def workspace(device: int, dtype_id: int, n: int):
+    need = _lib.lib().tf_reduce_workspace_bytes(0, dtype_id, n)
+    key = (device, dtype_id)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.zeros(max(need, 4096), dtype=torch.uint8, device="cuda:%d" % device)
+        _WS[key] = ws
+    return ws
+
+
+def _reduce(name, rop, ins, out=None):
+    planes = [_describe(name, p) for p in ins]
+    first = planes[0]
+    for p in planes[1:]:
+        if p.dtype != first.dtype:
+            raise ValueError("%s: planes mix %s and %s" % (name, first.dtype, p.dtype))
+        if p.n != first.n:
+            raise ValueError("%s: plane lengths differ (%d vs %d)" % (name, first.n, p.n))
+    if any(p.kind != "cuda" for p in planes):
+        raise ValueError("%s: reductions take CUDA tensors" % name)
+    if len({p.device for p in planes}) != 1:
+        raise ValueError("%s: planes live on different devices" % name)
+    dev = first.device
+    _lib.ensure_device(dev)
+    dt = _dtype_id(first.dtype)
+    tdt = torch.float64 if dt == _lib.TF_F64 else torch.float32
+    res = out if out is not None else torch.empty(2, dtype=tdt, device="cuda:%d" % dev)
+    if res.dtype != tdt or not res.is_cuda or res.numel() < 2:
+        raise ValueError("%s: out must be a 2-element CUDA tensor of the plane dtype" % name)
+    ws = workspace(dev, dt, first.n)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = _lib.lib().tf_reduce(_lib.ROP_IDS[rop], dt, first.n, planes[0].ptr,
+                                  planes[1].ptr if len(planes) > 1 else None,
+                                  res.data_ptr(), ws.data_ptr(), ws.numel(), stream)
+    _lib.check(rc, name)
+    if out is not None:
+        return out
+    v = res.cpu().tolist()
+    return Twofold(v[0], v[1])
+
+
+def vtsum(x, out=None):
+    """Twofold sum of a plane: lanes fold ``_tadd1`` from (x, +0); trees of ``_tadd``."""
+    return _reduce("vtsum", "sum", (x,), out)
+
+
+def vtsum2(x, out=None):
+    """Twofold sum of a TwofoldArray: lanes fold ``_tadd`` from (x0, x1)."""
+    x0, x1 = x
+    return _reduce("vtsum2", "sum2", (x0, x1), out)
+
+
+def vtdot(x, y, out=None):
+    """Twofold dot: lanes fold ``_tadd`` of ``_two_prod(x_i, y_i)``."""
+    return _reduce("vtdot", "dot", (x, y), out)
+
+
+def combine(partials, counts, out=None):
+    """Adjacent-pair ``_tadd`` tree over per-shard partials (g x 2 CUDA tensor)."""
+    p = partials.contiguous()
+    g = p.shape[0]
+    dt = _lib.TF_F64 if p.dtype == torch.float64 else _lib.TF_F32
+    res = out if out is not None else torch.empty(2, dtype=p.dtype, device=p.device)
+    c = (ctypes.c_int64 * max(g, 1))(*[int(v) for v in counts])
+    with torch.cuda.device(p.device):
+        stream = torch.cuda.current_stream(p.device).cuda_stream
+        rc = _lib.lib().tf_combine(dt, g, p.data_ptr(), c, res.data_ptr(), stream)
+    _lib.check(rc, "combine")
+    if out is not None:
+        return out
+    v = res.cpu().tolist()
+    return Twofold(v[0], v[1])
+
+
+def vthorner(coeffs, x, out):
+    """out = twofold Horner of Σ_k coeffs[k]·x^k (ascending powers) at every x_i."""
+    c = [float(v) for v in coeffs]
+    if not c:
+        raise ValueError("vthorner: need at least one coefficient")
+    r0, r1 = out
+    planes = _check("vthorner", (x,), (r0, r1))
+    first = planes[0]
+    if first.kind != "cuda":
+        raise ValueError("vthorner: planes must be CUDA tensors")
+    if first.n == 0:
+        return
+    dev = first.device
+    _lib.ensure_device(dev)
+    carr = (ctypes.c_double * len(c))(*c)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        rc = _lib.lib().tf_horner(_dtype_id(first.dtype), first.n, first.ptr, carr, len(c) - 1,
+                                  planes[1].ptr, planes[2].ptr, stream)
+    _lib.check(rc, "vthorner")
+
+
+def binomial_coeffs(degree=20):
+    """Coefficients of the expanded (x-1)^degree, ascending powers (exact in f64)."""
+    from math import comb
+
+    return [float((-1) ** (degree - k) * comb(degree, k)) for k in range(degree + 1)]
+
+
+__all__ = ["Twofold", "vtsum", "vtsum2", "vtdot", "vthorner", "combine", "geometry",
+           "tile_elems", "binomial_coeffs", "TwofoldArray"]

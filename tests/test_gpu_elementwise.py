@@ -1,0 +1,313 @@
+"""GPU parity of the elementwise kernels (run on a B200 via gpurun / the driver).
+
+Every comparison is bit-exact on both planes, NaN positions compared by isnan
+(x86 and NVIDIA NaN payloads differ; test_kernels.py:148-155 compares NaN the
+same way).  Sources of truth: the reference-generated goldens and the oracle.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+ELEM = np.load(GOLDEN / "elementwise.npz")
+NAMES = sorted({k.split("/")[0] for k in ELEM.files})
+DEV = "cuda:0"
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    if a.shape != b.shape:
+        return False
+    na, nb = np.isnan(a), np.isnan(b)
+    if not np.array_equal(na, nb):
+        return False
+    u = np.uint64 if a.dtype == np.float64 else np.uint32
+    return np.array_equal(a[~na].view(u), b[~nb].view(u))
+
+
+def first_mismatch(a, b):
+    u = np.uint64 if a.dtype == np.float64 else np.uint32
+    bad = np.flatnonzero((a.view(u) != b.view(u)) & ~(np.isnan(a) & np.isnan(b)))
+    return bad[:5]
+
+
+def run_device(name, ins, offset=0, offsets=None):
+    """Run one op on the device over copies of the host planes; optional
+    element offsets make the planes misaligned views."""
+    from paper_1401_6235_b200 import kernels as K
+
+    n = ins[0].shape[0]
+    dt = torch.float64 if ins[0].dtype == np.float64 else torch.float32
+    offs = offsets or [offset] * (len(ins) + 2)
+    planes = []
+    for k, p in enumerate(ins):
+        buf = torch.empty(n + offs[k], dtype=dt, device=DEV)
+        v = buf[offs[k]:]
+        v.copy_(torch.from_numpy(np.ascontiguousarray(p)))
+        planes.append(v)
+    outs = []
+    for k in range(2):
+        o = offs[len(ins) + k]
+        buf = torch.full((n + o,), 7.0, dtype=dt, device=DEV)
+        outs.append(buf[o:])
+    if name in K.RAW_OPS:
+        K.raw_loop(name)(*planes, *outs)
+    else:
+        spec = K.KERNELS[name]
+        if spec.arity == "22":
+            spec.func(K.TwofoldArray(planes[0], planes[1]), K.TwofoldArray(planes[2], planes[3]), K.TwofoldArray(*outs))
+        elif spec.arity == "21":
+            spec.func(K.TwofoldArray(planes[0], planes[1]), planes[2], K.TwofoldArray(*outs))
+        elif spec.arity == "11":
+            spec.func(planes[0], planes[1], K.TwofoldArray(*outs))
+        elif spec.arity == "u2":
+            spec.func(K.TwofoldArray(planes[0], planes[1]), K.TwofoldArray(*outs))
+        else:
+            spec.func(planes[0], K.TwofoldArray(*outs))
+    torch.cuda.synchronize()
+    return outs[0].cpu().numpy(), outs[1].cpu().numpy()
+
+
+def golden_inputs(name, fmt):
+    ins, k = [], 0
+    while "%s/%s/in%d" % (name, fmt, k) in ELEM.files:
+        ins.append(ELEM["%s/%s/in%d" % (name, fmt, k)])
+        k += 1
+    return ins
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+@pytest.mark.parametrize("name", NAMES)
+def test_device_matches_reference_golden(name, fmt):
+    ins = golden_inputs(name, fmt)
+    r0, r1 = run_device(name, ins)
+    w0, w1 = ELEM["%s/%s/out0" % (name, fmt)], ELEM["%s/%s/out1" % (name, fmt)]
+    assert bits_equal(r0, w0), (name, first_mismatch(r0, w0))
+    assert bits_equal(r1, w1), (name, first_mismatch(r1, w1))
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+@pytest.mark.parametrize("name", ["vtadd2", "vtdiv1", "vtsqrt1", "vtmul", "vtsqrt", "vpmul2"])
+def test_device_misaligned_views(name, fmt):
+    # common misalignment (scalar head + vector body + scalar tail) and mixed
+    # misalignments (scalar grid-stride path) must give the same bits
+    ins = golden_inputs(name, fmt)
+    w0, w1 = ELEM["%s/%s/out0" % (name, fmt)], ELEM["%s/%s/out1" % (name, fmt)]
+    for offset in (1, 3):
+        r0, r1 = run_device(name, ins, offset=offset)
+        assert bits_equal(r0, w0) and bits_equal(r1, w1), (name, offset)
+    mixed = [k % 3 for k in range(len(ins) + 2)]
+    r0, r1 = run_device(name, ins, offsets=mixed)
+    assert bits_equal(r0, w0) and bits_equal(r1, w1), (name, "mixed")
+
+
+def _config1(n, seed):
+    # BASELINE config 1: x0,y0 ~ U[-1,1]; x1 = x0*2^-53*U[-1,1], likewise y1
+    rng = np.random.default_rng(seed)
+    x0 = rng.uniform(-1, 1, n)
+    x1 = x0 * 2.0**-53 * rng.uniform(-1, 1, n)
+    y0 = rng.uniform(-1, 1, n)
+    y1 = y0 * 2.0**-53 * rng.uniform(-1, 1, n)
+    return x0, x1, y0, y1
+
+
+@pytest.mark.parametrize("name", ["vtadd2", "vtmul2"])
+def test_config1_bit_exact_vs_oracle(oracle, name):
+    ins = _config1(2**20, 1 if name == "vtadd2" else 2)
+    r0, r1 = run_device(name, ins)
+    w0, w1 = oracle.elementwise(name, *ins)
+    assert bits_equal(r0, w0) and bits_equal(r1, w1)
+
+
+def _config2_inputs(name, n, seed):
+    # BASELINE config 2 distributions (log-uniform heads, tails head*2^-53*U[-1,1])
+    rng = np.random.default_rng(seed)
+
+    def head(lo, hi, signed=True):
+        v = np.exp2(rng.uniform(lo, hi, n))
+        return v * rng.choice([-1.0, 1.0], n) if signed else v
+
+    def tail(h):
+        return h * 2.0**-53 * rng.uniform(-1, 1, n)
+
+    if name == "vtsqrt1":
+        x0 = head(-20, 20, signed=False)
+        return x0, tail(x0)
+    x0 = head(-20, 20)
+    y0 = head(-10, 10, signed=False) if name == "vtdiv2" else head(-20, 20)
+    return x0, tail(x0), y0, tail(y0)
+
+
+@pytest.mark.parametrize("name", ["vtadd2", "vtsub2", "vtmul2", "vtdiv2", "vtsqrt1"])
+def test_config2_ops_bit_exact_vs_oracle(oracle, name):
+    n = (1 << 22) + 5
+    ins = _config2_inputs(name, n, 20 + len(name))
+    r0, r1 = run_device(name, ins)
+    w0, w1 = oracle.elementwise(name, *ins)
+    assert bits_equal(r0, w0), first_mismatch(r0, w0)
+    assert bits_equal(r1, w1), first_mismatch(r1, w1)
+
+
+@pytest.mark.parametrize("name", ["vtadd2", "vtmul2", "vtdiv2"])
+def test_config3_f32_bit_exact_vs_oracle(oracle, name):
+    n = (1 << 22) + 3
+    rng = np.random.default_rng(33)
+    x0 = rng.uniform(-1, 1, n).astype(np.float32)
+    x1 = (x0 * np.float32(2.0**-24) * rng.uniform(-1, 1, n).astype(np.float32)).astype(np.float32)
+    if name == "vtdiv2":
+        y0 = rng.uniform(0.5, 2, n).astype(np.float32)
+    else:
+        y0 = rng.uniform(-1, 1, n).astype(np.float32)
+    y1 = (y0 * np.float32(2.0**-24) * rng.uniform(-1, 1, n).astype(np.float32)).astype(np.float32)
+    ins = (x0, x1, y0, y1)
+    r0, r1 = run_device(name, ins)
+    w0, w1 = oracle.elementwise(name, *ins)
+    assert bits_equal(r0, w0) and bits_equal(r1, w1)
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+def test_all_ops_random_wide_vs_oracle(oracle, fmt):
+    # every op at a size with many CTAs, wide exponents, subnormal-producing tails
+    from paper_1401_6235_b200 import kernels as K
+
+    dtype = np.float64 if fmt == "f64" else np.float32
+    n = 300_001
+    rng = np.random.default_rng(9)
+    me = 300 if fmt == "f64" else 40
+    for name in list(K.KERNELS) + ["div_rem", "sqrt_resid"]:
+        nin = {4: 4, 3: 3, 2: 2, 1: 1}[{"22": 4, "21": 3, "11": 2, "u2": 2, "u1": 1}.get(
+            K.KERNELS[name].arity if name in K.KERNELS else ("11" if name == "div_rem" else "u1"))]
+        with np.errstate(all="ignore"):
+            ins = []
+            for k in range(nin):
+                v = rng.uniform(1, 2, n) * np.exp2(rng.integers(-me, me, n)) * rng.choice([-1.0, 1.0], n)
+                if name in ("vtsqrt1", "vtsqrt", "sqrt_resid") and k == 0:
+                    v = np.abs(v)
+                ins.append(v.astype(dtype))
+        with np.errstate(all="ignore"):
+            w0, w1 = oracle.elementwise(name, *ins)
+        r0, r1 = run_device(name, ins)
+        assert bits_equal(r0, w0), (name, first_mismatch(r0, w0))
+        assert bits_equal(r1, w1), (name, first_mismatch(r1, w1))
+
+
+def test_host_planes_path_matches_oracle(oracle):
+    # numpy planes in and out: the reference's calling convention, staged through
+    # the device by tf_elementwise_host (several pipeline chunks)
+    from paper_1401_6235_b200 import kernels as K
+
+    n = 5 * (1 << 21) + 17
+    ins = _config2_inputs("vtdiv2", n, 4)
+    out = K.empty_twofold(n, np.float64, device="cpu")
+    K.vtdiv2(K.TwofoldArray(ins[0], ins[1]), K.TwofoldArray(ins[2], ins[3]), out)
+    w0, w1 = oracle.elementwise("vtdiv2", *ins)
+    assert bits_equal(out.value, w0) and bits_equal(out.error, w1)
+    # pinned host planes take the same path
+    outp = K.empty_twofold(n, np.float64, device="cpu", pin_memory=True)
+    K.vtdiv2(K.TwofoldArray(ins[0], ins[1]), K.TwofoldArray(ins[2], ins[3]), outp)
+    assert bits_equal(outp.value, w0) and bits_equal(outp.error, w1)
+
+
+# ---- the reference's test_kernels.py contract, re-run on device planes ----
+
+def _t(a):
+    return torch.as_tensor(np.asarray(a), device=DEV)
+
+
+def test_length_one_matches_reference_value():
+    from paper_1401_6235_b200 import kernels as K
+
+    x = K.TwofoldArray(_t([1.0]), _t([-(2.0**-53)]))
+    y = K.TwofoldArray(_t([2.0**-53]), _t([-(2.0**-106)]))
+    out = K.empty_twofold(1, torch.float64)
+    K.vtadd2(x, y, out)
+    # tadd((1,-2^-53),(2^-53,-2^-106)): TwoSum(1, 2^-53) = (1, 2^-53)
+    assert (out.value.item(), out.error.item()) == (1.0, (-(2.0**-53) + -(2.0**-106)) + 2.0**-53)
+
+
+def test_inputs_may_alias_each_other(oracle):
+    from paper_1401_6235_b200 import kernels as K
+
+    v = np.array([1.0, 2.0, 3.0])
+    e = np.array([2.0**-54, 0.0, -(2.0**-53)])
+    x = K.TwofoldArray(_t(v), _t(e))
+    out = K.empty_twofold(3, torch.float64)
+    K.vtadd2(x, x, out)
+    w0, w1 = oracle.elementwise("vtadd2", v, e, v, e)
+    assert bits_equal(out.value.cpu().numpy(), w0) and bits_equal(out.error.cpu().numpy(), w1)
+
+
+def test_specials_flow_through_kernels():
+    from paper_1401_6235_b200 import kernels as K
+
+    out = K.empty_twofold(3, torch.float64, K.CoupledArray)
+    K.vtdiv(_t([1.0, 0.0, -1.0]), _t([0.0, 0.0, np.inf]), out)
+    v, e = out.value.cpu().numpy(), out.error.cpu().numpy()
+    assert v[0] == np.inf and np.isnan(e[0])
+    assert np.isnan(v[1]) and np.isnan(e[1])
+    assert v[2] == 0.0 and np.signbit(v[2])
+    out = K.empty_twofold(1, torch.float64, K.CoupledArray)
+    K.vtsqrt(_t([-1.0]), out)
+    assert np.isnan(out.value.item()) and np.isnan(out.error.item())
+
+
+def test_dotted_kernel_outputs_are_coupled():
+    from paper_1401_6235_b200 import kernels as K
+
+    rng = np.random.default_rng(7)
+    a = rng.uniform(1, 2, 1000) * np.exp2(rng.integers(-3, 4, 1000)) * rng.choice([-1.0, 1.0], 1000)
+    b = rng.uniform(1, 2, 1000) * np.exp2(rng.integers(-3, 4, 1000)) * rng.choice([-1.0, 1.0], 1000)
+    out = K.empty_twofold(1000, torch.float64, K.CoupledArray)
+    for f in (K.vtadd, K.vtmul, K.vtdiv):
+        f(_t(a), _t(b), out)
+        v, e = out.value.cpu().numpy(), out.error.cpu().numpy()
+        assert np.all(np.abs(e) <= np.spacing(np.abs(v)) / 2)
+
+
+def test_empty_arrays_are_a_no_op():
+    from paper_1401_6235_b200 import kernels as K
+
+    x = K.TwofoldArray(torch.empty(0, dtype=torch.float64, device=DEV),
+                       torch.empty(0, dtype=torch.float64, device=DEV))
+    out = K.empty_twofold(0, torch.float64)
+    K.vtadd2(x, x, out)
+    assert out.value.shape == (0,)
+
+
+def test_device_validation_before_launch():
+    from paper_1401_6235_b200 import kernels as K
+
+    x = K.TwofoldArray(_t(np.ones(8)), _t(np.ones(8)))
+    out = K.TwofoldArray(torch.full((8,), 7.0, dtype=torch.float64, device=DEV),
+                         torch.full((8,), 7.0, dtype=torch.float64, device=DEV))
+    with pytest.raises(ValueError, match="alias"):
+        K.vtadd2(x, x, K.TwofoldArray(x.value, out.error))
+    with pytest.raises(ValueError, match="overlap"):
+        K.vtadd2(x, x, K.TwofoldArray(out.value, out.value))
+    with pytest.raises(ValueError, match="mix"):
+        K.vtadd2(x, K.TwofoldArray(np.ones(8), np.ones(8)), out)
+    with pytest.raises(ValueError, match="lengths differ"):
+        K.vtadd2(x, K.TwofoldArray(x.value[:4], x.error[:4]), out)
+    torch.cuda.synchronize()
+    assert torch.all(out.value == 7.0) and torch.all(out.error == 7.0)
+
+
+def test_selftest_and_dotted_baselines():
+    from paper_1401_6235_b200 import _lib
+
+    assert _lib.lib().tf_selftest(0) == 0
+    n = 1001
+    rng = np.random.default_rng(1)
+    x = _t(rng.uniform(1, 2, n))
+    y = _t(rng.uniform(1, 2, n))
+    r = torch.empty_like(x)
+    s = torch.cuda.current_stream().cuda_stream
+    for base, ref in ((0, x + y), (1, x * y), (2, x / y), (3, torch.sqrt(x)), (4, x)):
+        assert _lib.lib().tf_dotted(base, 1, n, x.data_ptr(), y.data_ptr(), r.data_ptr(), s) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(r, ref), base

@@ -1,0 +1,231 @@
+"""GPU parity of the reductions and Horner (B200).
+
+Reductions: bit-exact against the reference-generated goldens at the device
+geometry and against the oracle at larger sizes; the error bound
+|(z0+z1) - exact| <= 4u·Σ|terms| against the exact accumulator; bit-identical
+results for every shard count G (shards reduced on the device and combined
+with tf_combine, as the multi-GPU path does).
+"""
+
+import json
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda:0"
+
+RED = np.load(GOLDEN / "reductions.npz")
+RED_CASES = json.loads((GOLDEN / "reductions.json").read_text())
+HORNER = np.load(GOLDEN / "horner.npz")
+
+
+def _t(a):
+    return torch.as_tensor(np.ascontiguousarray(a), device=DEV)
+
+
+def _device_reduce(rop, x, y=None, offset=0):
+    from paper_1401_6235_b200 import reduce as R
+
+    def put(a):
+        if offset == 0:
+            return _t(a)
+        buf = torch.empty(a.shape[0] + offset, dtype=_t(a[:1]).dtype, device=DEV)
+        buf[offset:].copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        return buf[offset:]
+
+    if rop == "sum":
+        z = R.vtsum(put(x))
+    elif rop == "sum2":
+        z = R.vtsum2((put(x), put(y)))
+    else:
+        z = R.vtdot(put(x), put(y))
+    return z
+
+
+def _geom(dtype):
+    from paper_1401_6235_b200 import reduce as R
+
+    return R.geometry(dtype)
+
+
+def _regen(case):
+    dtype = np.float64 if case["fmt"] == "f64" else np.float32
+    if case["stored"]:
+        return RED[case["key"] + "/x"], RED[case["key"] + "/y"]
+    n = case["n"]
+    rng = np.random.default_rng(case["seed"])
+    if case["kind"] == "uniform":
+        x, y = rng.uniform(-1, 1, n), rng.uniform(-1, 1, n)
+    else:
+        x = rng.uniform(-1, 1, n) * np.exp2(rng.integers(-30, 31, n))
+        y = rng.uniform(-1, 1, n) * np.exp2(rng.integers(-30, 31, n))
+    x, y = x.astype(dtype), y.astype(dtype)
+    if case["rop"] == "sum2":
+        y = (x * dtype(2.0**-30) * y).astype(dtype)
+    return x, y
+
+
+DEVICE_CASES = [c for c in RED_CASES if tuple(c["geom"]) in ((2, 256, 128), (4, 256, 128))]
+
+
+def test_device_geometry_is_the_golden_geometry():
+    assert _geom(np.float64) == (2, 256, 128)
+    assert _geom(np.float32) == (4, 256, 128)
+    assert len(DEVICE_CASES) >= 40
+
+
+@pytest.mark.parametrize("case", DEVICE_CASES, ids=[c["key"] for c in DEVICE_CASES])
+def test_device_reduction_matches_reference_golden(case):
+    x, y = _regen(case)
+    z = _device_reduce(case["rop"], x, y)
+    want = RED[case["key"] + "/z"]
+    got = np.array([z.value, z.error], dtype=want.dtype)
+    assert np.array_equal(got.view(np.uint64 if want.dtype == np.float64 else np.uint32),
+                          want.view(np.uint64 if want.dtype == np.float64 else np.uint32)), (got, want)
+
+
+@pytest.mark.parametrize("offset", [1, 3])
+@pytest.mark.parametrize("rop", ["sum", "sum2", "dot"])
+def test_device_reduction_unaligned_planes(oracle, rop, offset):
+    rng = np.random.default_rng(offset)
+    n = 3 * 65536 + 999
+    x = rng.uniform(-1, 1, n)
+    y = rng.uniform(-1, 1, n)
+    z = _device_reduce(rop, x, y, offset=offset)
+    w = oracle.reduce(rop, x, None if rop == "sum" else y, geometry=_geom(np.float64))
+    assert (z.value, z.error) == (float(w[0]), float(w[1]))
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+@pytest.mark.parametrize("rop", ["sum", "sum2", "dot"])
+def test_device_reduction_large_vs_oracle(oracle, rop, fmt):
+    dtype = np.float64 if fmt == "f64" else np.float32
+    rng = np.random.default_rng(11)
+    n = (1 << 24) + 12345
+    x = (rng.uniform(-1, 1, n) * np.exp2(rng.integers(-20, 21, n))).astype(dtype)
+    y = (rng.uniform(-1, 1, n) * np.exp2(rng.integers(-20, 21, n))).astype(dtype)
+    z = _device_reduce(rop, x, y)
+    w = oracle.reduce(rop, x, None if rop == "sum" else y, geometry=_geom(dtype))
+    assert (z.value, z.error) == (float(w[0]), float(w[1]))
+
+
+def _ill_dot(n, cond, seed):
+    from paper_1401_6235_b200 import _lib
+
+    x = np.empty(n)
+    y = np.empty(n)
+    assert _lib.lib().tf_gen_dot_host(n, cond, seed, x.ctypes.data, y.ctypes.data) == 0
+    return x, y
+
+
+@pytest.mark.parametrize("cond", [1e8, 1e16, 1e24])
+def test_ill_conditioned_dot_and_sum_bound(oracle, cond):
+    n = 1 << 21
+    x, y = _ill_dot(n, cond, 7)
+    z = _device_reduce("dot", x, y)
+    w = oracle.reduce("dot", x, y, geometry=_geom(np.float64))
+    assert (z.value, z.error) == (float(w[0]), float(w[1]))
+    ok, err, s, t = oracle.bound_ok(z.value, z.error, "dot", x, y)
+    assert ok, (float(err), float(t))
+    achieved = float(2 * t / abs(s)) if s else float("inf")
+    assert achieved > cond / 1e4  # the generator reaches the intended conditioning
+    # the sum form: terms are the exact TwoProd pieces of the products
+    p, e = oracle.elementwise("vtmul", x, y)
+    terms = np.empty(2 * n)
+    terms[0::2] = p
+    terms[1::2] = e
+    zs = _device_reduce("sum", terms)
+    ws = oracle.reduce("sum", terms, geometry=_geom(np.float64))
+    assert (zs.value, zs.error) == (float(ws[0]), float(ws[1]))
+    ok, err, s2, t2 = oracle.bound_ok(zs.value, zs.error, "sum", terms)
+    assert ok and s2 == s
+
+
+@pytest.mark.parametrize("G", [2, 3, 4, 8])
+def test_shard_count_invariance(G):
+    # the multi-GPU data path on one device: each shard reduced by the device
+    # kernel, partials combined by tf_combine, must equal the one-shard result
+    from paper_1401_6235_b200 import dist as D
+    from paper_1401_6235_b200 import reduce as R
+
+    rng = np.random.default_rng(G)
+    n = 9 * 65536 + 4321
+    x = rng.uniform(-1, 1, n) * np.exp2(rng.integers(-40, 41, n))
+    X = _t(x)
+    whole = R.vtsum(X)
+    L = R.tile_elems(np.float64)
+    parts = torch.zeros((G, 2), dtype=torch.float64, device=DEV)
+    counts = []
+    for r in range(G):
+        lo, hi = D.shard_tiles(n, G, r, L)
+        counts.append(hi - lo)
+        if hi > lo:
+            R.vtsum(X[lo:hi], out=parts[r])
+    z = R.combine(parts, counts)
+    assert (z.value, z.error) == (whole.value, whole.error)
+
+
+def test_empty_and_single():
+    from paper_1401_6235_b200 import reduce as R
+
+    z = R.vtsum(torch.empty(0, dtype=torch.float64, device=DEV))
+    assert (z.value, z.error) == (0.0, 0.0)
+    z = R.vtsum(_t(np.array([-0.0])))
+    assert z.value == 0.0 and np.signbit(z.value)  # seeded from (x, +0), not (+0, +0)
+    z = R.vtdot(_t(np.array([3.0])), _t(np.array([1.0 / 3.0])))
+    assert z.value == 3.0 * (1.0 / 3.0)
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+@pytest.mark.parametrize("deg", [20, 5, 1, 0])
+def test_horner_matches_reference_golden(fmt, deg):
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+
+    x = HORNER["%s/deg%d/x" % (fmt, deg)]
+    c = HORNER["%s/deg%d/c" % (fmt, deg)]
+    dt = torch.float64 if fmt == "f64" else torch.float32
+    out = K.empty_twofold(x.shape[0], dt)
+    R.vthorner(c, _t(x), out)
+    w0, w1 = HORNER["%s/deg%d/out0" % (fmt, deg)], HORNER["%s/deg%d/out1" % (fmt, deg)]
+    u = np.uint64 if fmt == "f64" else np.uint32
+    assert np.array_equal(out.value.cpu().numpy().view(u), w0.view(u))
+    assert np.array_equal(out.error.cpu().numpy().view(u), w1.view(u))
+
+
+def test_horner_config5_vs_oracle_and_flag(oracle):
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+
+    n = (1 << 22) + 7
+    x = np.random.default_rng(5).uniform(0.9, 1.1, n)
+    c = R.binomial_coeffs(20)
+    out = K.empty_twofold(n, torch.float64)
+    R.vthorner(c, _t(x), out)
+    w0, w1 = oracle.horner(c, x)
+    z0, z1 = out.value.cpu().numpy(), out.error.cpu().numpy()
+    assert np.array_equal(z0.view(np.uint64), w0.view(np.uint64))
+    assert np.array_equal(z1.view(np.uint64), w1.view(np.uint64))
+    nz = z0 != 0
+    flag = np.abs(z1[nz]) >= 0.5 * np.abs(z0[nz])
+    assert flag.mean() > 0.99  # z1 flags the catastrophic cancellation near x=1
+
+
+def test_horner_generic_degree_vs_oracle(oracle):
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+
+    n = 100_003
+    rng = np.random.default_rng(8)
+    x = rng.uniform(-2, 2, n)
+    c = list(rng.uniform(-1, 1, 37))
+    out = K.empty_twofold(n, torch.float64)
+    R.vthorner(c, _t(x), out)
+    w0, w1 = oracle.horner(c, x)
+    assert np.array_equal(out.value.cpu().numpy().view(np.uint64), w0.view(np.uint64))
+    assert np.array_equal(out.error.cpu().numpy().view(np.uint64), w1.view(np.uint64))
