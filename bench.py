@@ -1,0 +1,671 @@
+"""Benchmark of the twofold hot path on B200 — driver contract (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload config2|config1|config3|config4|config5] [--n N]
+
+Default workload = BASELINE.json configs[1] (the headline): the full fp64 op set
+vtadd2, vtsub2, vtmul2, vtdiv2, vtsqrt1 at n = 2^28 elements per GPU (weak
+scaling: every rank owns an independent 2^28-element shard of a global array of
+N·2^28; no collective on the data path).  One step = one pass of the five
+kernels.  Inputs are seeded synthetic planes with BASELINE's distributions,
+generated on the device (tf_fill) before timing; each plane is 2 GiB, far larger
+than the 126 MB L2, so no flush is needed between steps.
+
+Keys beyond the base contract:
+  roofline      dominant kernel: algorithmic bytes / CUDA-event launch time vs
+                MEASURED_PEAKS.json hbm_gbs (burst copy figure)
+  cpu_baseline  the CPU oracle port (oracle/, all host threads) on a bounded
+                sample of the same workload, rank 0 at N=1 only
+  e2e           the same metric through the public API with pinned HOST planes
+                (kernels.vtadd2(numpy...) -> tf_elementwise_host), H2D and D2H inside
+  per_op        per-kernel CUDA-event times and GB/s
+  clocks        NVML SM clock + event reasons sampled during the timed region
+
+--impl reference times the reference algorithm's CPU implementation — the oracle
+port (the numba reference cannot travel to the GPU box) — on all host threads.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "twofold elem-ops/s & achieved HBM GB/s (fp64) at 1/2/4/8 B200 vs CPU oracle"
+
+# op -> (inputs, bytes/elem f64)
+NIN = {"vtadd2": 4, "vtsub2": 4, "vtmul2": 4, "vtdiv2": 4, "vtsqrt1": 2}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config2",
+                    choices=["config1", "config2", "config3", "config4", "config5"])
+    ap.add_argument("--n", type=int, default=0, help="elements per GPU (default: the config's)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 25,
+                    help="elements per op in the CPU baseline sample")
+    return ap.parse_args()
+
+
+def env_rank():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------
+# workloads: each returns a list of Op(name, launch(), algorithmic bytes, units)
+
+
+class Op:
+    def __init__(self, name, launch, nbytes, units, host_call=None, h2d=0, d2h=0, kernel=None):
+        self.name, self.launch, self.nbytes, self.units = name, launch, nbytes, units
+        self.host_call, self.h2d, self.d2h = host_call, h2d, d2h
+        self.kernel = kernel or name
+
+
+def _fill(t, kind, seed, offset, lo, hi, head=None):
+    import torch
+
+    from paper_1401_6235_b200 import _lib
+
+    dt = _lib.TF_F64 if t.dtype == torch.float64 else _lib.TF_F32
+    rc = _lib.lib().tf_fill(dt, kind, t.numel(), seed, offset, lo, hi,
+                            head.data_ptr() if head is not None else None, t.data_ptr(),
+                            torch.cuda.current_stream().cuda_stream)
+    _lib.check(rc, "tf_fill")
+
+
+def _pinned_copy(t):
+    import torch
+
+    h = torch.empty(t.numel(), dtype=t.dtype, pin_memory=True)
+    h.copy_(t)
+    return h.numpy()
+
+
+def workload_elementwise(names, dtype, n, rank, dists, want_host):
+    """dists: name -> list of (kind, lo, hi) per input plane (kind 3 = tail of plane 0/2)."""
+    import torch
+
+    from paper_1401_6235_b200 import kernels as K
+
+    dev = torch.cuda.current_device()
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+    esz = 8 if dtype == np.float64 else 4
+    cache = {}
+    ops = []
+    out = K.empty_twofold(n, tdt, device=dev)
+    host_out = None
+    if want_host:
+        host_out = K.TwofoldArray(_pinned_copy(out.value), _pinned_copy(out.error))
+    hcache = {}
+    for j, name in enumerate(names):
+        planes = []
+        keys = []
+        for k, (kind, lo, hi) in enumerate(dists[name]):
+            # plane position is part of the key: x and y never share a buffer;
+            # a tail plane is keyed by the head it is derived from
+            key = (k, kind, lo, hi, keys[k - 1] if kind == 3 else None)
+            keys.append(key)
+            if key in cache:
+                planes.append(cache[key])
+                continue
+            t = torch.empty(n, dtype=tdt, device=dev)
+            seed = 1000 + 17 * len(cache)
+            _fill(t, kind, seed, rank * n, lo, hi, planes[k - 1] if kind == 3 else None)
+            cache[key] = t
+            planes.append(t)
+        spec = K.KERNELS[name]
+        nin = len(planes)
+        nbytes = (nin + 2) * esz * n
+        raw = spec.loop
+        args = list(planes) + [out.value, out.error]
+        host_args = None
+        if want_host:
+            hp = []
+            for key, p in zip(keys, planes):
+                if key not in hcache:
+                    hcache[key] = _pinned_copy(p)
+                hp.append(hcache[key])
+            if spec.arity == "22":
+                host_args = (K.TwofoldArray(hp[0], hp[1]), K.TwofoldArray(hp[2], hp[3]), host_out)
+            elif spec.arity == "21":
+                host_args = (K.TwofoldArray(hp[0], hp[1]), hp[2], host_out)
+            elif spec.arity == "11":
+                host_args = (hp[0], hp[1], host_out)
+            elif spec.arity == "u2":
+                host_args = (K.TwofoldArray(hp[0], hp[1]), host_out)
+            else:
+                host_args = (hp[0], host_out)
+        ops.append(Op(name, (lambda raw=raw, args=args: raw(*args)), nbytes, n,
+                      host_call=(lambda f=spec.func, a=host_args: f(*a)) if want_host else None,
+                      h2d=nin * esz * n, d2h=2 * esz * n))
+    return ops, cache
+
+
+def config2_dists():
+    head = (1, -20.0, 20.0)
+    tail = (3, -53.0, 0.0)
+    div = (2, -10.0, 10.0)
+    pos = (2, -20.0, 20.0)
+    return {"vtadd2": [head, tail, head, tail], "vtsub2": [head, tail, head, tail],
+            "vtmul2": [head, tail, head, tail], "vtdiv2": [head, tail, div, tail],
+            "vtsqrt1": [pos, tail]}
+
+
+def config3_dists():
+    head = (0, -1.0, 1.0)
+    tail = (3, -24.0, 0.0)
+    div = (0, 0.5, 2.0)
+    return {"vtadd2": [head, tail, head, tail], "vtmul2": [head, tail, head, tail],
+            "vtdiv2": [head, tail, div, tail]}
+
+
+def config1_dists():
+    head = (0, -1.0, 1.0)
+    tail = (3, -53.0, 0.0)
+    return {"vtadd2": [head, tail, head, tail], "vtmul2": [head, tail, head, tail]}
+
+
+# --------------------------------------------------------------------------
+# measurement helpers
+
+
+class ClockSampler:
+    """NVML SM clock + clock-event reasons, sampled every 10 ms in a thread."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_ev.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        return json.loads(p.read_text()).get(kernel)
+    except Exception:
+        return None
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3):
+    """Oracle port (plain C, OpenMP, all host threads) on a bounded sample."""
+    from oracle import oracle as o
+
+    rng = np.random.default_rng(99)
+    planes = {}
+    total_units = 0
+    t_total = 0.0
+    nt = os.cpu_count() or 1
+    out = (np.zeros(n_sample, dtype), np.zeros(n_sample, dtype))
+    for name in ops_names:
+        ins = dists_host(name, rng, n_sample)
+        o.elementwise(name, *ins, nthreads=nt, out=out)  # warm-up (thread pool)
+        best = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            o.elementwise(name, *ins, nthreads=nt, out=out)
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        t_total += best
+        total_units += n_sample
+        planes[name] = best
+    return total_units / t_total, nt, planes
+
+
+def host_dists(workload):
+    """numpy generators with the same distributions as the device fill (CPU arms)."""
+
+    def c2(name, rng, n):
+        def head(lo, hi, signed=True):
+            v = np.exp2(rng.uniform(lo, hi, n))
+            return v * rng.choice([-1.0, 1.0], n) if signed else v
+
+        def tail(h, p=-53):
+            return h * 2.0**p * rng.uniform(-1, 1, n)
+
+        if name == "vtsqrt1":
+            x0 = head(-20, 20, False)
+            return [x0, tail(x0)]
+        x0 = head(-20, 20)
+        y0 = head(-10, 10, False) if name == "vtdiv2" else head(-20, 20)
+        return [x0, tail(x0), y0, tail(y0)]
+
+    def c3(name, rng, n):
+        f = np.float32
+        x0 = rng.uniform(-1, 1, n).astype(f)
+        y0 = (rng.uniform(0.5, 2, n) if name == "vtdiv2" else rng.uniform(-1, 1, n)).astype(f)
+        t = lambda h: (h * f(2.0**-24) * rng.uniform(-1, 1, n).astype(f)).astype(f)  # noqa: E731
+        return [x0, t(x0), y0, t(y0)]
+
+    def c1(name, rng, n):
+        x0 = rng.uniform(-1, 1, n)
+        y0 = rng.uniform(-1, 1, n)
+        return [x0, x0 * 2.0**-53 * rng.uniform(-1, 1, n), y0, y0 * 2.0**-53 * rng.uniform(-1, 1, n)]
+
+    return {"config1": c1, "config2": c2, "config3": c3}[workload]
+
+
+WL = {
+    "config1": dict(names=["vtadd2", "vtmul2"], dtype=np.float64, n=1 << 20, dists=config1_dists,
+                    desc="BASELINE configs[0]: f64 vtadd2+vtmul2, n=2^20 (parity config, L2-resident)"),
+    "config2": dict(names=["vtadd2", "vtsub2", "vtmul2", "vtdiv2", "vtsqrt1"], dtype=np.float64,
+                    n=1 << 28, dists=config2_dists,
+                    desc="BASELINE configs[1]: f64 vtadd2/vtsub2/vtmul2/vtdiv2/vtsqrt1, n=2^28 per GPU"),
+    "config3": dict(names=["vtadd2", "vtmul2", "vtdiv2"], dtype=np.float32, n=1 << 30,
+                    dists=config3_dists,
+                    desc="BASELINE configs[2]: f32 vtadd2/vtmul2/vtdiv2, n=2^30 per GPU"),
+}
+
+
+# --------------------------------------------------------------------------
+# arms
+
+
+def run_reference(args, rank, world):
+    """CPU reference arm: the oracle port on all host threads (rank 0 only)."""
+    if rank != 0:
+        return 0
+    wl = WL.get(args.workload, WL["config2"])
+    n_sample = min(args.n or wl["n"], args.cpu_sample)
+    from oracle import oracle as o
+
+    gen = host_dists(args.workload if args.workload in WL else "config2")
+    rng = np.random.default_rng(7)
+    inputs = {name: gen(name, rng, n_sample) for name in wl["names"]}
+    nt = os.cpu_count() or 1
+    out = (np.zeros(n_sample, wl["dtype"]), np.zeros(n_sample, wl["dtype"]))
+
+    def step():
+        for name in wl["names"]:
+            o.elementwise(name, *inputs[name], nthreads=nt, out=out)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    units = len(wl["names"]) * n_sample * args.steps
+    value = units / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "elem-ops/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64" if wl["dtype"] == np.float64 else "f32",
+        "data": "synthetic (seeded numpy, BASELINE distributions)",
+        "config": {"workload": wl["desc"], "sample_elems_per_op": n_sample,
+                   "ops": wl["names"]},
+        "cpu_baseline": {"value": value, "unit": "elem-ops/s", "cores": nt, "kind": "port",
+                         "sample": "%d elements per op x %d ops per step, oracle/twofold_oracle.c "
+                                   "(OpenMP, -O3 -march=x86-64-v3, no contraction)"
+                                   % (n_sample, len(wl["names"]))},
+        "e2e": {"value": value, "unit": "elem-ops/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_elementwise(args, rank, world, local):
+    import torch
+
+    from paper_1401_6235_b200 import _lib
+
+    wl = WL[args.workload]
+    n = args.n or wl["n"]
+    dtype = wl["dtype"]
+    esz = 8 if dtype == np.float64 else 4
+    _lib.ensure_device(local)
+    want_host = not args.no_e2e
+    ops, _ = workload_elementwise(wl["names"], dtype, n, rank, wl["dists"](), want_host)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        for op in ops:
+            op.launch()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in ops] for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for s in range(K):
+            for j, op in enumerate(ops):
+                ev[s][j][0].record(stream)
+                op.launch()
+                ev[s][j][1].record(stream)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    elapsed_ms = max_over_ranks(start.elapsed_time(end), world)
+    launches = K * len(ops)
+
+    per_op = {}
+    for j, op in enumerate(ops):
+        ts = [ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(K)]
+        avg = sum(ts) / K
+        per_op[op.name] = {"ms": avg, "gbs": op.nbytes / (avg * 1e-3) / 1e9,
+                           "bytes": op.nbytes, "share": sum(ts) / elapsed_ms}
+    dom = max(per_op, key=lambda k: per_op[k]["ms"])
+    peak, peak_src = measured_peak()
+    units_per_step = sum(op.units for op in ops)
+    value = world * units_per_step * K / (elapsed_ms * 1e-3)
+    bytes_per_step = sum(op.nbytes for op in ops)
+
+    # end-to-end through the public API with pinned host planes
+    e2e = None
+    if want_host:
+        for op in ops:  # warm the host pipeline (staging buffers, streams)
+            op.host_call()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            for op in ops:
+                op.host_call()
+        dt = time.perf_counter() - t0
+        barrier(world)
+        dt = max_over_ranks(dt, world)
+        e2e = {"value": world * units_per_step * args.e2e_steps / dt, "unit": "elem-ops/s",
+               "h2d_bytes_per_step": sum(op.h2d for op in ops),
+               "d2h_bytes_per_step": sum(op.d2h for op in ops),
+               "steps": args.e2e_steps,
+               "path": "kernels.<op>(pinned numpy planes) -> tf_elementwise_host "
+                       "(chunked H2D / kernel / D2H pipeline)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gen = host_dists(args.workload)
+        v, nt, per = cpu_baseline_elementwise(wl["names"], gen, dtype,
+                                              min(n, args.cpu_sample))
+        cpu = {"value": v, "unit": "elem-ops/s", "cores": nt, "kind": "port",
+               "sample": "%d elements per op over %s (best of 3 per op), oracle/twofold_oracle.c "
+                         "OpenMP on %d threads" % (min(n, args.cpu_sample), "/".join(wl["names"]), nt)}
+
+    if rank == 0:
+        d = per_op[dom]
+        line = {
+            "metric": METRIC, "value": value, "unit": "elem-ops/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": elapsed_ms / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64" if dtype == np.float64 else "f32",
+            "data": "synthetic (seeded, device-generated with BASELINE distributions)",
+            "config": {"workload": wl["desc"], "n_per_gpu": n, "ops": wl["names"],
+                       "layout": "split SoA planes", "l2": "inputs %d MiB per plane >> 126 MB L2; no flush"
+                       % (n * esz >> 20)},
+            "hbm_gbs": world * bytes_per_step * K / (elapsed_ms * 1e-3) / 1e9,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak,
+                         "unit": "GB/s", "frac": d["gbs"] / peak, "traffic": ncu_traffic(dom),
+                         "algorithmic_bytes": d["bytes"], "peak_source": peak_src},
+            "per_op": per_op,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_config4(args, rank, world, local):
+    """f64 vtdot + vtsum over an ill-conditioned ORO-style dot (n = 2^30 per GPU),
+    per-GPU canonical tree, then all-gather + tf_combine across GPUs."""
+    import torch
+
+    from paper_1401_6235_b200 import _lib, dist as D, reduce as R
+
+    n = args.n or (1 << 30)
+    _lib.ensure_device(local)
+    x = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    y = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    rc = _lib.lib().tf_gen_dot_host(n, 1e16, 4242 + rank, x.data_ptr(), y.data_ptr())
+    _lib.check(rc, "tf_gen_dot_host")
+    X, Y = x.cuda(), y.cuda()
+    L = R.tile_elems(np.float64)
+    n_glob = n * world
+    part = torch.empty(2, dtype=torch.float64, device="cuda")
+    part2 = torch.empty(2, dtype=torch.float64, device="cuda")
+    res = torch.empty(2, dtype=torch.float64, device="cuda")
+
+    def step():
+        R.vtdot(X, Y, out=part)
+        R.vtsum(X, out=part2)
+        if world > 1:
+            allp = D.gather_partials(part)
+            R.combine(allp, D.shard_counts(n_glob, world, L), out=res)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    K = args.steps
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for s in range(K):
+            ev[s][0].record(stream)
+            R.vtdot(X, Y, out=part)
+            ev[s][1].record(stream)
+            R.vtsum(X, out=part2)
+            if world > 1:
+                allp = D.gather_partials(part)
+                R.combine(allp, D.shard_counts(n_glob, world, L), out=res)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    elapsed_ms = max_over_ranks(start.elapsed_time(end), world)
+    dot_ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    peak, src = measured_peak()
+    value = world * 2 * n * K / (elapsed_ms * 1e-3)
+    # e2e: pinned host planes -> device -> reduce -> 16-byte result back
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        Xh = x.to("cuda", non_blocking=True)
+        Yh = y.to("cuda", non_blocking=True)
+        z = R.vtdot(Xh, Yh)
+        z2 = R.vtsum(Xh)
+    dt = max_over_ranks(time.perf_counter() - t0, world)
+    del z, z2
+    if rank == 0:
+        gbs = 16 * n / (dot_ms * 1e-3) / 1e9
+        line = {
+            "metric": METRIC + " [config4: vtdot+vtsum]", "value": value, "unit": "elem-ops/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": elapsed_ms / K,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (ORO-style ill-conditioned dot, cond 1e16, seeded)",
+            "config": {"workload": "BASELINE configs[3]: f64 vtdot + vtsum, n=2^30 per GPU",
+                       "n_per_gpu": n},
+            "roofline": {"bound": "hbm", "kernel": "vtdot", "achieved": gbs, "peak": peak,
+                         "unit": "GB/s", "frac": gbs / peak, "traffic": ncu_traffic("vtdot"),
+                         "algorithmic_bytes": 16 * n, "peak_source": src},
+            "e2e": {"value": world * 2 * n * args.e2e_steps / dt, "unit": "elem-ops/s",
+                    "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 32},
+            "gpu_launches": K * (2 + (1 if world > 1 else 0)),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_config5(args, rank, world, local):
+    """f64 twofold Horner of the expanded (x-1)^20 at n = 2^26 points per GPU."""
+    import torch
+
+    from paper_1401_6235_b200 import _lib, kernels as Kmod, reduce as R
+
+    n = args.n or (1 << 26)
+    _lib.ensure_device(local)
+    x = torch.empty(n, dtype=torch.float64, device="cuda")
+    _fill(x, 0, 555, rank * n, 0.9, 1.1)
+    out = Kmod.empty_twofold(n, torch.float64)
+    c = R.binomial_coeffs(20)
+    for _ in range(args.warmup):
+        R.vthorner(c, x, out)
+    import ctypes
+
+    pi, pm = ctypes.c_double(), ctypes.c_double()
+    _lib.check(_lib.lib().tf_fp64_peak(local, ctypes.byref(pi), ctypes.byref(pm)), "fp64_peak")
+    fp64_peak = pi.value / (pm.value * 1e-3)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    K = args.steps
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for _ in range(K):
+            R.vthorner(c, x, out)
+        end.record(stream)
+        torch.cuda.synchronize()
+    barrier(world)
+    elapsed_ms = max_over_ranks(start.elapsed_time(end), world)
+    per_ms = elapsed_ms / K
+    instr = 220.0 * n
+    achieved = instr / (per_ms * 1e-3)
+    value = world * n * K / (elapsed_ms * 1e-3)
+    if rank == 0:
+        line = {
+            "metric": "twofold Horner points/s (fp64, (x-1)^20)", "value": value, "unit": "points/s",
+            "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": per_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic x ~ U[0.9,1.1] (seeded, device-generated)",
+            "config": {"workload": "BASELINE configs[4]: twofold Horner (x-1)^20, n=2^26 per GPU",
+                       "n_per_gpu": n},
+            "roofline": {"bound": "fp64", "kernel": "vthorner", "achieved": achieved / 1e12,
+                         "peak": fp64_peak / 1e12, "unit": "T FP64 instr/s",
+                         "frac": achieved / fp64_peak, "traffic": ncu_traffic("vthorner"),
+                         "algorithmic_instr": instr,
+                         "peak_source": "measured live: tf_fp64_peak (independent DFMA chains)"},
+            "gpu_launches": K,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = env_rank()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        if args.workload == "config4":
+            rc = run_config4(args, rank, world, local)
+        elif args.workload == "config5":
+            rc = run_config5(args, rank, world, local)
+        else:
+            rc = run_elementwise(args, rank, world, local)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())
