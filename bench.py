@@ -64,6 +64,14 @@ def parse():
     return ap.parse_args()
 
 
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    if os.environ.get("RANK", "0") == "0":
+        print("[bench %7.1fs] %s" % (time.perf_counter() - _T0, msg), file=sys.stderr, flush=True)
+
+
 def env_rank():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -134,6 +142,7 @@ def workload_elementwise(names, dtype, n, rank, dists, want_host):
             _fill(t, kind, seed, rank * n, lo, hi, planes[k - 1] if kind == 3 else None)
             cache[key] = t
             planes.append(t)
+        log("  %s: device planes ready" % name)
         spec = K.KERNELS[name]
         nin = len(planes)
         nbytes = (nin + 2) * esz * n
@@ -156,6 +165,7 @@ def workload_elementwise(names, dtype, n, rank, dists, want_host):
                 host_args = (K.TwofoldArray(hp[0], hp[1]), host_out)
             else:
                 host_args = (hp[0], host_out)
+            log("  %s: pinned host planes ready" % name)
         ops.append(Op(name, (lambda raw=raw, args=args: raw(*args)), nbytes, n,
                       host_call=(lambda f=spec.func, a=host_args: f(*a)) if want_host else None,
                       h2d=nin * esz * n, d2h=2 * esz * n))
@@ -406,8 +416,10 @@ def run_elementwise(args, rank, world, local):
     esz = 8 if dtype == np.float64 else 4
     _lib.ensure_device(local)
     want_host = not args.no_e2e
+    log("generating inputs n=%d" % n)
     ops, _ = workload_elementwise(wl["names"], dtype, n, rank, wl["dists"](), want_host)
     torch.cuda.synchronize()
+    log("inputs ready")
     stream = torch.cuda.current_stream()
 
     for _ in range(args.warmup):
@@ -433,6 +445,7 @@ def run_elementwise(args, rank, world, local):
     barrier(world)
     elapsed_ms = max_over_ranks(start.elapsed_time(end), world)
     launches = K * len(ops)
+    log("timed region done: %.3f ms/step" % (elapsed_ms / K))
 
     per_op = {}
     for j, op in enumerate(ops):
@@ -449,8 +462,10 @@ def run_elementwise(args, rank, world, local):
     # end-to-end through the public API with pinned host planes
     e2e = None
     if want_host:
+        log("e2e warm-up")
         for op in ops:  # warm the host pipeline (staging buffers, streams)
             op.host_call()
+        log("e2e timed")
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
@@ -468,6 +483,7 @@ def run_elementwise(args, rank, world, local):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        log("cpu baseline")
         gen = host_dists(args.workload)
         v, nt, per = cpu_baseline_elementwise(wl["names"], gen, dtype,
                                               min(n, args.cpu_sample))
@@ -475,6 +491,7 @@ def run_elementwise(args, rank, world, local):
                "sample": "%d elements per op over %s (best of 3 per op), oracle/twofold_oracle.c "
                          "OpenMP on %d threads" % (min(n, args.cpu_sample), "/".join(wl["names"]), nt)}
 
+    log("done")
     if rank == 0:
         d = per_op[dom]
         line = {

@@ -18,7 +18,7 @@ TF_OK, TF_EINVAL, TF_ECUDA, TF_ENOMEM, TF_ESELFTEST = 0, -1, -2, -3, -4
 TF_F32, TF_F64 = 0, 1
 ROP_IDS = {"sum": 0, "sum2": 1, "dot": 2}
 
-_lock = threading.Lock()
+_lock = threading.RLock()
 _lib = None
 _selftested = set()
 
@@ -96,10 +96,11 @@ def ensure_device(device: int) -> None:
     """Run the device self-test (the _fused_or_die analogue) once per device."""
     if device in _selftested:
         return
+    L = lib()
     with _lock:
         if device in _selftested:
             return
-        rc = lib().tf_selftest(int(device))
+        rc = L.tf_selftest(int(device))
         if rc != TF_OK:
             raise RuntimeError("twofold device self-test failed on cuda:%d: %s"
                                % (device, last_error()))
