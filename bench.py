@@ -267,6 +267,30 @@ def ncu_traffic(kernel):
         return None
 
 
+def link_probe(nbytes=1 << 30):
+    """Measured host<->device duplex bandwidth (concurrent H2D + D2H of pinned
+    buffers, GB/s): the roofline of the e2e (host-plane) path."""
+    import torch
+
+    h = torch.empty(nbytes // 8, dtype=torch.float64, pin_memory=True)
+    h2 = torch.empty_like(h, pin_memory=True)
+    d = torch.empty(nbytes // 8, dtype=torch.float64, device="cuda")
+    d2 = torch.empty_like(d)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    best = 0.0
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+        torch.cuda.synchronize()
+        best = max(best, 2 * nbytes / (time.perf_counter() - t) / 1e9)
+    del h, h2, d, d2
+    return best
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
@@ -474,7 +498,12 @@ def run_elementwise(args, rank, world, local):
         dt = time.perf_counter() - t0
         barrier(world)
         dt = max_over_ranks(dt, world)
+        link = link_probe()
+        moved = sum(op.h2d + op.d2h for op in ops) * args.e2e_steps / dt / 1e9
         e2e = {"value": world * units_per_step * args.e2e_steps / dt, "unit": "elem-ops/s",
+               "roofline": {"bound": "pcie", "achieved": moved, "peak": link, "unit": "GB/s",
+                            "frac": moved / link,
+                            "peak_source": "measured live: concurrent pinned H2D+D2H copies"},
                "h2d_bytes_per_step": sum(op.h2d for op in ops),
                "d2h_bytes_per_step": sum(op.d2h for op in ops),
                "steps": args.e2e_steps,
