@@ -91,15 +91,9 @@ class Op:
 
 
 def _fill(t, kind, seed, offset, lo, hi, head=None):
-    import torch
+    from paper_1401_6235_b200 import workloads
 
-    from paper_1401_6235_b200 import _lib
-
-    dt = _lib.TF_F64 if t.dtype == torch.float64 else _lib.TF_F32
-    rc = _lib.lib().tf_fill(dt, kind, t.numel(), seed, offset, lo, hi,
-                            head.data_ptr() if head is not None else None, t.data_ptr(),
-                            torch.cuda.current_stream().cuda_stream)
-    _lib.check(rc, "tf_fill")
+    workloads.fill(t, kind, seed, offset, lo, hi, head)
 
 
 def _pinned_copy(t):
@@ -110,38 +104,27 @@ def _pinned_copy(t):
     return h.numpy()
 
 
-def workload_elementwise(names, dtype, n, rank, dists, want_host):
-    """dists: name -> list of (kind, lo, hi) per input plane (kind 3 = tail of plane 0/2)."""
+def workload_elementwise(names, dtype, n, rank, config, want_host):
+    """Device planes (workloads.PlaneSet, BASELINE distributions) + launchers;
+    pinned host copies for the e2e path."""
     import torch
 
     from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import workloads as WLs
 
     dev = torch.cuda.current_device()
     tdt = torch.float64 if dtype == np.float64 else torch.float32
     esz = 8 if dtype == np.float64 else 4
-    cache = {}
+    ps = WLs.PlaneSet(config, n, tdt, dev, offset=rank * n)
     ops = []
     out = K.empty_twofold(n, tdt, device=dev)
     host_out = None
     if want_host:
         host_out = K.TwofoldArray(_pinned_copy(out.value), _pinned_copy(out.error))
     hcache = {}
-    for j, name in enumerate(names):
-        planes = []
-        keys = []
-        for k, (kind, lo, hi) in enumerate(dists[name]):
-            # plane position is part of the key: x and y never share a buffer;
-            # a tail plane is keyed by the head it is derived from
-            key = (k, kind, lo, hi, keys[k - 1] if kind == 3 else None)
-            keys.append(key)
-            if key in cache:
-                planes.append(cache[key])
-                continue
-            t = torch.empty(n, dtype=tdt, device=dev)
-            seed = 1000 + 17 * len(cache)
-            _fill(t, kind, seed, rank * n, lo, hi, planes[k - 1] if kind == 3 else None)
-            cache[key] = t
-            planes.append(t)
+    for name in names:
+        planes = ps.planes(name)
+        keys = ps.keys[name]
         log("  %s: device planes ready" % name)
         spec = K.KERNELS[name]
         nin = len(planes)
@@ -169,31 +152,7 @@ def workload_elementwise(names, dtype, n, rank, dists, want_host):
         ops.append(Op(name, (lambda raw=raw, args=args: raw(*args)), nbytes, n,
                       host_call=(lambda f=spec.func, a=host_args: f(*a)) if want_host else None,
                       h2d=nin * esz * n, d2h=2 * esz * n))
-    return ops, cache
-
-
-def config2_dists():
-    head = (1, -20.0, 20.0)
-    tail = (3, -53.0, 0.0)
-    div = (2, -10.0, 10.0)
-    pos = (2, -20.0, 20.0)
-    return {"vtadd2": [head, tail, head, tail], "vtsub2": [head, tail, head, tail],
-            "vtmul2": [head, tail, head, tail], "vtdiv2": [head, tail, div, tail],
-            "vtsqrt1": [pos, tail]}
-
-
-def config3_dists():
-    head = (0, -1.0, 1.0)
-    tail = (3, -24.0, 0.0)
-    div = (0, 0.5, 2.0)
-    return {"vtadd2": [head, tail, head, tail], "vtmul2": [head, tail, head, tail],
-            "vtdiv2": [head, tail, div, tail]}
-
-
-def config1_dists():
-    head = (0, -1.0, 1.0)
-    tail = (3, -53.0, 0.0)
-    return {"vtadd2": [head, tail, head, tail], "vtmul2": [head, tail, head, tail]}
+    return ops, ps
 
 
 # --------------------------------------------------------------------------
@@ -304,7 +263,8 @@ def max_over_ranks(x, world):
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -368,13 +328,12 @@ def host_dists(workload):
 
 
 WL = {
-    "config1": dict(names=["vtadd2", "vtmul2"], dtype=np.float64, n=1 << 20, dists=config1_dists,
+    "config1": dict(names=["vtadd2", "vtmul2"], dtype=np.float64, n=1 << 20,
                     desc="BASELINE configs[0]: f64 vtadd2+vtmul2, n=2^20 (parity config, L2-resident)"),
     "config2": dict(names=["vtadd2", "vtsub2", "vtmul2", "vtdiv2", "vtsqrt1"], dtype=np.float64,
-                    n=1 << 28, dists=config2_dists,
+                    n=1 << 28,
                     desc="BASELINE configs[1]: f64 vtadd2/vtsub2/vtmul2/vtdiv2/vtsqrt1, n=2^28 per GPU"),
     "config3": dict(names=["vtadd2", "vtmul2", "vtdiv2"], dtype=np.float32, n=1 << 30,
-                    dists=config3_dists,
                     desc="BASELINE configs[2]: f32 vtadd2/vtmul2/vtdiv2, n=2^30 per GPU"),
 }
 
@@ -441,7 +400,7 @@ def run_elementwise(args, rank, world, local):
     _lib.ensure_device(local)
     want_host = not args.no_e2e
     log("generating inputs n=%d" % n)
-    ops, _ = workload_elementwise(wl["names"], dtype, n, rank, wl["dists"](), want_host)
+    ops, _ = workload_elementwise(wl["names"], dtype, n, rank, args.workload, want_host)
     torch.cuda.synchronize()
     log("inputs ready")
     stream = torch.cuda.current_stream()
@@ -693,11 +652,19 @@ def main():
         return run_reference(args, rank, world)
     import torch
 
+    if os.environ.get("BENCH_DIST_BACKEND", "nccl") != "nccl":
+        local = 0  # dry run: every rank on cuda:0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # BENCH_DIST_BACKEND=gloo: host-side dry run of the multi-rank path on one
+        # GPU (no kernel waits on another rank; never used for reported numbers)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     try:
         if args.workload == "config4":
             rc = run_config4(args, rank, world, local)

@@ -62,11 +62,12 @@ def gather_partials(partial, group=None):
     out = torch.empty((world, 2), dtype=partial.dtype, device=partial.device)
     if dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(out, partial.reshape(2).contiguous(), group=group)
-    else:
-        parts = [torch.empty(2, dtype=partial.dtype, device=partial.device) for _ in range(world)]
-        dist.all_gather(parts, partial.reshape(2).contiguous(), group=group)
+    else:  # gloo (CPU tests, single-GPU dry runs): gather through host tensors
+        src = partial.reshape(2).contiguous().cpu()
+        parts = [torch.empty(2, dtype=partial.dtype) for _ in range(world)]
+        dist.all_gather(parts, src, group=group)
         for r in range(world):
-            out[r] = parts[r]
+            out[r] = parts[r].to(out.device)
     return out
 
 

@@ -20,6 +20,7 @@ GOLDEN = Path(__file__).resolve().parent / "golden"
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
     config.addinivalue_line("markers", "slow: long-running CPU test")
+    config.addinivalue_line("markers", "fullsize: GPU parity at BASELINE.json's full sizes")
 
 
 def pytest_collection_modifyitems(config, items):

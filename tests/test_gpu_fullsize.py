@@ -1,0 +1,112 @@
+"""Parity at BASELINE.json's full sizes (B200).
+
+Every element of every output plane is compared bit-exactly with the oracle:
+config 2 (f64 x5 ops, n=2^28), config 3 (f32 x3 ops, n=2^30), config 4 (dot and
+sum, n=2^30, ill-conditioned: bit-exact in the canonical order and inside the
+4u·Σ|terms| bound against the exact accumulator) and config 5 (Horner, 2^26
+points, plus the cancellation flag).  Inputs are the bench's own device-
+generated planes (paper_1401_6235_b200.workloads), copied to the host.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = [pytest.mark.gpu, pytest.mark.fullsize]
+
+
+def _host(t):
+    return t.cpu().numpy()
+
+
+def _bits_equal_chunked(a, b, chunk=1 << 26):
+    u = np.uint64 if a.dtype == np.float64 else np.uint32
+    for i in range(0, a.shape[0], chunk):
+        x, y = a[i:i + chunk], b[i:i + chunk]
+        nx, ny = np.isnan(x), np.isnan(y)
+        if not np.array_equal(nx, ny):
+            return False
+        if not np.array_equal(x.view(u)[~nx], y.view(u)[~ny]):
+            return False
+    return True
+
+
+def _run_config(oracle, config, names, n, dtype):
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import workloads as W
+
+    ps = W.PlaneSet(config, n, dtype, 0)
+    out = K.empty_twofold(n, dtype)
+    npdt = np.float64 if dtype == torch.float64 else np.float32
+    ref = (np.empty(n, npdt), np.empty(n, npdt))
+    for name in names:
+        planes = ps.planes(name)
+        K.KERNELS[name].loop(*planes, out.value, out.error)
+        torch.cuda.synchronize()
+        ins = [_host(p) for p in planes]
+        oracle.elementwise(name, *ins, out=ref)
+        z0, z1 = _host(out.value), _host(out.error)
+        assert _bits_equal_chunked(z0, ref[0]), (config, name, "value plane")
+        assert _bits_equal_chunked(z1, ref[1]), (config, name, "error plane")
+        del ins, z0, z1
+
+
+def test_config2_full_size_bit_exact(oracle):
+    _run_config(oracle, "config2", ["vtadd2", "vtsub2", "vtmul2", "vtdiv2", "vtsqrt1"],
+                1 << 28, torch.float64)
+
+
+def test_config3_full_size_bit_exact(oracle):
+    _run_config(oracle, "config3", ["vtadd2", "vtmul2", "vtdiv2"], 1 << 30, torch.float32)
+
+
+def test_config1_bit_exact(oracle):
+    _run_config(oracle, "config1", ["vtadd2", "vtmul2"], 1 << 20, torch.float64)
+
+
+def test_config4_full_size_dot_and_sum(oracle):
+    from paper_1401_6235_b200 import _lib
+    from paper_1401_6235_b200 import reduce as R
+
+    n = 1 << 30
+    x = np.empty(n)
+    y = np.empty(n)
+    assert _lib.lib().tf_gen_dot_host(n, 1e16, 4242, x.ctypes.data, y.ctypes.data) == 0
+    X, Y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    geom = R.geometry(np.float64)
+    z = R.vtdot(X, Y)
+    w = oracle.reduce("dot", x, y, geometry=geom)
+    assert (z.value, z.error) == (float(w[0]), float(w[1]))
+    ok, err, s, t = oracle.bound_ok(z.value, z.error, "dot", x, y)
+    assert ok, (float(err), float(t))
+    cond = float(2 * t / abs(s))
+    assert cond > 1e12, cond  # genuinely ill-conditioned at full size
+    # plain double dot in the same order is far off; the twofold is not
+    rel_plain = abs(float(z.value) - float(s)) / abs(float(s))
+    rel_tf = float(err / abs(s))
+    assert rel_tf < 1e-10 and rel_tf < rel_plain
+    zs = R.vtsum(X)
+    ws = oracle.reduce("sum", x, geometry=geom)
+    assert (zs.value, zs.error) == (float(ws[0]), float(ws[1]))
+    ok, err, s2, t2 = oracle.bound_ok(zs.value, zs.error, "sum", x)
+    assert ok
+
+
+def test_config5_full_size_horner(oracle):
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+    from paper_1401_6235_b200 import workloads as W
+
+    n = 1 << 26
+    x = W.fill(torch.empty(n, dtype=torch.float64, device="cuda"), W.UNIFORM, 555, 0, 0.9, 1.1)
+    out = K.empty_twofold(n, torch.float64)
+    c = R.binomial_coeffs(20)
+    R.vthorner(c, x, out)
+    torch.cuda.synchronize()
+    xh = _host(x)
+    w0, w1 = oracle.horner(c, xh)
+    z0, z1 = _host(out.value), _host(out.error)
+    assert _bits_equal_chunked(z0, w0) and _bits_equal_chunked(z1, w1)
+    nz = z0 != 0
+    assert (np.abs(z1[nz]) >= 0.5 * np.abs(z0[nz])).mean() > 0.99
