@@ -1,7 +1,7 @@
 """Benchmark of the twofold hot path on B200 — driver contract (one JSON line).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload config2|config1|config3|config4|config5] [--n N]
+                    [--workload config2|config1|config3|config4|config5] [--elems N]
 
 Default workload = BASELINE.json configs[1] (the headline): the full fp64 op set
 vtadd2, vtsub2, vtmul2, vtdiv2, vtsqrt1 at n = 2^28 elements per GPU (weak
@@ -55,7 +55,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="config2",
                     choices=["config1", "config2", "config3", "config4", "config5"])
-    ap.add_argument("--n", type=int, default=0, help="elements per GPU (default: the config's)")
+    ap.add_argument("--elems", dest="n", type=int, default=0,
+                    help="elements per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
