@@ -1,0 +1,272 @@
+// interleaved.cu — the 24 elementwise ops over the INTERLEAVED (AoS) layout,
+// plus split<->interleaved conversion kernels.
+//
+// Interleaved: a twofold operand or result is one array of n (value, error)
+// pairs, the paper's twofold<T> struct {value, error}.  Scalar
+// (non-twofold) operands stay plain 1-D planes.  A binary twofold op streams 3
+// arrays instead of 6 planes; the bytes per element are the same
+// ((NIN+2)*sizeof(T)), and so is the arithmetic: apply<T,OP> from tf_math.cuh,
+// i.e. the reference cores (arith.py:61-218) bit for bit.
+//
+// Vector body: each step covers E = 16/sizeof(T) elements — one 16-byte load
+// per plain plane, two per interleaved operand, two 16-byte stores for the
+// result.  Requires 16-byte aligned arrays; otherwise a scalar grid-stride path
+// (same launch).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "tf_math.cuh"
+
+namespace tf {
+
+template <class T>
+struct ILArgs {
+  const T* a;  // x: pairs if twofold (22, 21, u2), else plain
+  const T* b;  // y: pairs if 22, plain if 21/11, unused for unary
+  T* out;      // pairs
+};
+
+template <class T, int OP>
+__device__ __forceinline__ void il_gather(const ILArgs<T>& p, int64_t i, T* v) {
+  constexpr int AR = OpInfo<OP>::ARITY;
+  if constexpr (AR == 22) {
+    v[0] = ld_stream(p.a + 2 * i);
+    v[1] = ld_stream(p.a + 2 * i + 1);
+    v[2] = ld_stream(p.b + 2 * i);
+    v[3] = ld_stream(p.b + 2 * i + 1);
+  } else if constexpr (AR == 21) {
+    v[0] = ld_stream(p.a + 2 * i);
+    v[1] = ld_stream(p.a + 2 * i + 1);
+    v[2] = ld_stream(p.b + i);
+  } else if constexpr (AR == 11) {
+    v[0] = ld_stream(p.a + i);
+    v[1] = ld_stream(p.b + i);
+  } else if constexpr (AR == 2) {
+    v[0] = ld_stream(p.a + 2 * i);
+    v[1] = ld_stream(p.a + 2 * i + 1);
+  } else {
+    v[0] = ld_stream(p.a + i);
+  }
+}
+
+template <class T, int OP>
+__global__ void __launch_bounds__(256) ew_il_kernel(ILArgs<T> p, int64_t n, int vec) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  constexpr int AR = OpInfo<OP>::ARITY;
+  constexpr int E = Vec16<T>::N;
+  using V = typename Vec16<T>::type;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nvec = vec ? n / E : 0;
+
+  for (int64_t j = gtid; j < nvec; j += gstride) {
+    // E elements: element e of step j is index j*E + e
+    T v[E][NIN];
+    if constexpr (AR == 22 || AR == 21 || AR == 2) {
+      const V* xa = reinterpret_cast<const V*>(p.a) + 2 * j;  // 2E scalars = E pairs
+      V r0 = ld_stream(xa), r1 = ld_stream(xa + 1);
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        const V& r = (2 * e < E) ? r0 : r1;
+        v[e][0] = lane<T>(r, (2 * e) % E);
+        v[e][1] = lane<T>(r, (2 * e + 1) % E);
+      }
+    } else {
+      V r = ld_stream(reinterpret_cast<const V*>(p.a) + j);
+#pragma unroll
+      for (int e = 0; e < E; e++) v[e][0] = lane<T>(r, e);
+    }
+    if constexpr (AR == 22) {
+      const V* yb = reinterpret_cast<const V*>(p.b) + 2 * j;
+      V r0 = ld_stream(yb), r1 = ld_stream(yb + 1);
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        const V& r = (2 * e < E) ? r0 : r1;
+        v[e][2] = lane<T>(r, (2 * e) % E);
+        v[e][3] = lane<T>(r, (2 * e + 1) % E);
+      }
+    } else if constexpr (AR == 21) {
+      V r = ld_stream(reinterpret_cast<const V*>(p.b) + j);
+#pragma unroll
+      for (int e = 0; e < E; e++) v[e][2] = lane<T>(r, e);
+    } else if constexpr (AR == 11) {
+      V r = ld_stream(reinterpret_cast<const V*>(p.b) + j);
+#pragma unroll
+      for (int e = 0; e < E; e++) v[e][1] = lane<T>(r, e);
+    }
+    V o0, o1;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      P<T> z = apply<T, OP>(v[e]);
+      if (2 * e < E) {
+        set_lane<T>(o0, (2 * e) % E, z.a);
+        set_lane<T>(o0, (2 * e + 1) % E, z.b);
+      } else {
+        set_lane<T>(o1, (2 * e) % E, z.a);
+        set_lane<T>(o1, (2 * e + 1) % E, z.b);
+      }
+    }
+    V* o = reinterpret_cast<V*>(p.out) + 2 * j;
+    st_stream(o, o0);
+    st_stream(o + 1, o1);
+  }
+  // scalar remainder (or everything, when unaligned)
+  for (int64_t i = nvec * E + gtid; i < n; i += gstride) {
+    T v[NIN];
+    il_gather<T, OP>(p, i, v);
+    P<T> z = apply<T, OP>(v);
+    st_stream(p.out + 2 * i, z.a);
+    st_stream(p.out + 2 * i + 1, z.b);
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) interleave_kernel(const T* __restrict__ v,
+                                                         const T* __restrict__ e,
+                                                         T* __restrict__ out, int64_t n,
+                                                         int vec) {
+  using Vt = typename Vec16<T>::type;
+  constexpr int E = Vec16<T>::N;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nvec = vec ? n / E : 0;
+  for (int64_t j = gtid; j < nvec; j += gstride) {
+    Vt a = ld_stream(reinterpret_cast<const Vt*>(v) + j);
+    Vt b = ld_stream(reinterpret_cast<const Vt*>(e) + j);
+    Vt o0, o1;
+#pragma unroll
+    for (int k = 0; k < E; k++) {
+      Vt& o = (2 * k < E) ? o0 : o1;
+      set_lane<T>(o, (2 * k) % E, lane<T>(a, k));
+      set_lane<T>(o, (2 * k + 1) % E, lane<T>(b, k));
+    }
+    Vt* po = reinterpret_cast<Vt*>(out) + 2 * j;
+    st_stream(po, o0);
+    st_stream(po + 1, o1);
+  }
+  for (int64_t i = nvec * E + gtid; i < n; i += gstride) {
+    st_stream(out + 2 * i, ld_stream(v + i));
+    st_stream(out + 2 * i + 1, ld_stream(e + i));
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) deinterleave_kernel(const T* __restrict__ in,
+                                                           T* __restrict__ v, T* __restrict__ e,
+                                                           int64_t n, int vec) {
+  using Vt = typename Vec16<T>::type;
+  constexpr int E = Vec16<T>::N;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nvec = vec ? n / E : 0;
+  for (int64_t j = gtid; j < nvec; j += gstride) {
+    const Vt* pi = reinterpret_cast<const Vt*>(in) + 2 * j;
+    Vt r0 = ld_stream(pi), r1 = ld_stream(pi + 1);
+    Vt a, b;
+#pragma unroll
+    for (int k = 0; k < E; k++) {
+      const Vt& r = (2 * k < E) ? r0 : r1;
+      set_lane<T>(a, k, lane<T>(r, (2 * k) % E));
+      set_lane<T>(b, k, lane<T>(r, (2 * k + 1) % E));
+    }
+    st_stream(reinterpret_cast<Vt*>(v) + j, a);
+    st_stream(reinterpret_cast<Vt*>(e) + j, b);
+  }
+  for (int64_t i = nvec * E + gtid; i < n; i += gstride) {
+    st_stream(v + i, ld_stream(in + 2 * i));
+    st_stream(e + i, ld_stream(in + 2 * i + 1));
+  }
+}
+
+// ---- dispatch ------------------------------------------------------------------
+
+struct IlEntry {
+  const void* fn;
+  int occ;
+};
+
+template <class T, int OP>
+IlEntry make_il() {
+  return IlEntry{reinterpret_cast<const void*>(&ew_il_kernel<T, OP>), 0};
+}
+template <class T, int... OPS>
+struct IlTable {
+  static IlEntry* get() {
+    static IlEntry t[] = {make_il<T, OPS>()...};
+    return t;
+  }
+};
+static IlEntry* il_table(int dtype) {
+  if (dtype == TF_F64)
+    return IlTable<double, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19,
+                   20, 21, 22, 23>::get();
+  return IlTable<float, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
+                 21, 22, 23>::get();
+}
+
+static int64_t grid_for(int64_t work, int occ) {
+  int64_t blocks = (work + 255) / 256;
+  const int64_t cap = (int64_t)sm_count() * (occ > 0 ? occ : 4);
+  if (blocks > cap) blocks = cap;
+  return blocks < 1 ? 1 : blocks;
+}
+
+int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* out,
+              cudaStream_t s) {
+  if (op < 0 || op >= TF_NUM_OPS) return fail(TF_EINVAL, "tf_elementwise_il: unknown op id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, "tf_elementwise_il: planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, "tf_elementwise_il: negative length");
+  if (n == 0) return TF_OK;
+  static const int nin_of[TF_NUM_OPS] = {4, 4, 4, 4, 3, 3, 3, 3, 2, 2, 2, 2,
+                                         2, 1, 4, 4, 4, 4, 3, 3, 3, 3, 2, 1};
+  const bool binary = nin_of[op] >= 2 && op != TF_VTSQRT1;
+  if (!a || !out || (binary && !b)) return fail(TF_EINVAL, "tf_elementwise_il: null array");
+  IlEntry& ent = il_table(dtype)[op];
+  if (!ent.occ) {
+    int o = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ent.fn, 256, 0);
+    if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_il: occupancy");
+    ent.occ = o > 0 ? o : 1;
+  }
+  int vec = aligned16(a) && aligned16(out) && (!binary || aligned16(b));
+  const int E = dtype == TF_F64 ? 2 : 4;
+  ILArgs<double> p{static_cast<const double*>(a), static_cast<const double*>(b ? b : a),
+                   static_cast<double*>(out)};
+  const int64_t blocks = grid_for(vec ? n / E : n, ent.occ);
+  void* args[] = {&p, &n, &vec};
+  return cuda_status(cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, s),
+                     "tf_elementwise_il: launch");
+}
+
+int convert_launch(int to_interleaved, int dtype, int64_t n, const void* a, const void* b,
+                   void* c, cudaStream_t s) {
+  if ((dtype != TF_F32 && dtype != TF_F64) || n < 0)
+    return fail(TF_EINVAL, "tf_interleave: bad arguments");
+  if (n == 0) return TF_OK;
+  const int E = dtype == TF_F64 ? 2 : 4;
+  if (to_interleaved) {  // a = value, b = error, c = pairs
+    if (!a || !b || !c) return fail(TF_EINVAL, "tf_interleave: null array");
+    int vec = aligned16(a) && aligned16(b) && aligned16(c);
+    const int64_t blocks = grid_for(vec ? n / E : n, 8);
+    if (dtype == TF_F64)
+      interleave_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
+          (const double*)a, (const double*)b, (double*)c, n, vec);
+    else
+      interleave_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float*)a, (const float*)b,
+                                                                 (float*)c, n, vec);
+  } else {  // a = pairs, b = value out, c = error out
+    if (!a || !b || !c) return fail(TF_EINVAL, "tf_deinterleave: null array");
+    int vec = aligned16(a) && aligned16(b) && aligned16(c);
+    const int64_t blocks = grid_for(vec ? n / E : n, 8);
+    if (dtype == TF_F64)
+      deinterleave_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
+          (const double*)a, (double*)const_cast<void*>(b), (double*)c, n, vec);
+    else
+      deinterleave_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(
+          (const float*)a, (float*)const_cast<void*>(b), (float*)c, n, vec);
+  }
+  return launch_status(to_interleaved ? "tf_interleave" : "tf_deinterleave");
+}
+
+}  // namespace tf

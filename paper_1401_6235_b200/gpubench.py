@@ -177,8 +177,26 @@ def _dotted_launcher(name, dt, n, x, y, r):
     return launch
 
 
-def run_bench(plan=None, repetitions=5, device=0):
-    """Measure every plan cell plus the dotted baselines (bench.py:226-267)."""
+def _il_args(spec, planes):
+    from . import interleaved as IL
+    from .kernels import TwofoldArray
+
+    ar = spec.arity
+    if ar == "22":
+        return (IL.from_split(TwofoldArray(planes[0], planes[1])),
+                IL.from_split(TwofoldArray(planes[2], planes[3])))
+    if ar == "21":
+        return (IL.from_split(TwofoldArray(planes[0], planes[1])), planes[2])
+    if ar == "u2":
+        return (IL.from_split(TwofoldArray(planes[0], planes[1])), None)
+    if ar == "11":
+        return (planes[0], planes[1])
+    return (planes[0], None)
+
+
+def run_bench(plan=None, repetitions=5, device=0, layout="split"):
+    """Measure every plan cell plus the dotted baselines (bench.py:226-267).
+    layout="interleaved" times the (n, 2) pair-array kernels instead."""
     if repetitions < 3:
         raise ValueError("repetitions must be >= 3 to filter noise")
     if plan is None:
@@ -218,9 +236,17 @@ def run_bench(plan=None, repetitions=5, device=0):
             dotted[(name, fmt, size)] = mega
         for op, spec in cells:
             planes = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in inputs(op, fmt, n)]
-            out = [torch.empty(n, dtype=tdt, device="cuda") for _ in range(2)]
-            loop = spec.loop
-            iters, best = _measure(lambda: loop(*planes, *out), repetitions)
+            if layout == "interleaved":
+                from . import interleaved as IL
+
+                xa, ya = _il_args(spec, planes)
+                po = torch.empty((n, 2), dtype=tdt, device="cuda")
+                il = IL.KERNELS[op].launch
+                iters, best = _measure(lambda: il(xa, ya, po), repetitions)
+            else:
+                out = [torch.empty(n, dtype=tdt, device="cuda") for _ in range(2)]
+                loop = spec.loop
+                iters, best = _measure(lambda: loop(*planes, *out), repetitions)
             mega = n * iters / best / 1e6
             bpe = (_NIN[spec.arity] + 2) * esz
             gbps = bpe * n * iters / best / 1e9
@@ -264,9 +290,11 @@ def main(argv=None):
     ap.add_argument("--format", dest="formats", help="comma-separated f32,f64 (default: both)")
     ap.add_argument("--csv", help="also write records to this CSV path")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--layout", choices=["split", "interleaved"], default="split")
     a = ap.parse_args(argv)
     sp = lambda t: None if t is None else [s for s in t.split(",") if s]  # noqa: E731
-    recs = run_bench(make_plan(sp(a.ops), sp(a.formats), sp(a.sizes)), repetitions=a.reps)
+    recs = run_bench(make_plan(sp(a.ops), sp(a.formats), sp(a.sizes)), repetitions=a.reps,
+                     layout=a.layout)
     print(format_table(recs), end="")
     if a.csv:
         write_csv(recs, a.csv)

@@ -1,0 +1,138 @@
+"""Interleaved (AoS) layout: same bits as the split layout and the reference
+goldens, for every op and both dtypes; conversions round-trip exactly."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from conftest import GOLDEN  # noqa: E402
+
+ELEM = np.load(GOLDEN / "elementwise.npz")
+NAMES = sorted({k.split("/")[0] for k in ELEM.files})
+ARITY = {}
+
+
+def _arity(name):
+    from paper_1401_6235_b200 import kernels as K
+
+    if name == "div_rem":
+        return "11"
+    if name == "sqrt_resid":
+        return "u1"
+    return K.KERNELS[name].arity
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    na, nb = np.isnan(a), np.isnan(b)
+    if a.shape != b.shape or not np.array_equal(na, nb):
+        return False
+    u = np.uint64 if a.dtype == np.float64 else np.uint32
+    return np.array_equal(a[~na].view(u), b[~nb].view(u))
+
+
+def _pairs(v, e, offset=0):
+    dt = torch.float64 if v.dtype == np.float64 else torch.float32
+    host = np.stack([v, e], axis=1)
+    if offset == 0:
+        return torch.from_numpy(np.ascontiguousarray(host)).cuda()
+    buf = torch.empty(host.size + offset, dtype=dt, device="cuda")
+    view = buf[offset:].view(-1, 2)
+    view.copy_(torch.from_numpy(host))
+    return view
+
+
+def _plane(v, offset=0):
+    if offset == 0:
+        return torch.from_numpy(np.ascontiguousarray(v)).cuda()
+    dt = torch.float64 if v.dtype == np.float64 else torch.float32
+    buf = torch.empty(v.shape[0] + offset, dtype=dt, device="cuda")
+    buf[offset:].copy_(torch.from_numpy(v))
+    return buf[offset:]
+
+
+def _run(name, fmt, offset=0):
+    from paper_1401_6235_b200 import interleaved as IL
+
+    ar = _arity(name)
+    ins = []
+    k = 0
+    while "%s/%s/in%d" % (name, fmt, k) in ELEM.files:
+        ins.append(ELEM["%s/%s/in%d" % (name, fmt, k)])
+        k += 1
+    n = ins[0].shape[0]
+    dt = torch.float64 if fmt == "f64" else torch.float32
+    if ar == "22":
+        args = (_pairs(ins[0], ins[1], offset), _pairs(ins[2], ins[3], offset))
+    elif ar == "21":
+        args = (_pairs(ins[0], ins[1], offset), _plane(ins[2], offset))
+    elif ar == "11":
+        args = (_plane(ins[0], offset), _plane(ins[1], offset))
+    elif ar == "u2":
+        args = (_pairs(ins[0], ins[1], offset),)
+    else:
+        args = (_plane(ins[0], offset),)
+    if offset:
+        buf = torch.full((2 * n + offset,), 7.0, dtype=dt, device="cuda")
+        out = buf[offset:].view(-1, 2)
+    else:
+        out = torch.full((n, 2), 7.0, dtype=dt, device="cuda")
+    IL.KERNELS[name](*args, out)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    return o[:, 0].copy(), o[:, 1].copy()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+@pytest.mark.parametrize("name", NAMES)
+def test_interleaved_matches_reference_golden(name, fmt):
+    for offset in (0, 1):
+        r0, r1 = _run(name, fmt, offset)
+        assert bits_equal(r0, ELEM["%s/%s/out0" % (name, fmt)]), (name, offset)
+        assert bits_equal(r1, ELEM["%s/%s/out1" % (name, fmt)]), (name, offset)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_conversions_round_trip(dtype):
+    from paper_1401_6235_b200 import interleaved as IL
+    from paper_1401_6235_b200 import kernels as K
+
+    for n in (0, 1, 7, 1 << 20 | 3):
+        v = torch.randn(n, dtype=dtype, device="cuda")
+        e = torch.randn(n, dtype=dtype, device="cuda") * 1e-17
+        p = IL.from_split(K.TwofoldArray(v, e))
+        assert torch.equal(p[:, 0], v) and torch.equal(p[:, 1], e)
+        back = IL.to_split(p)
+        assert torch.equal(back.value, v) and torch.equal(back.error, e)
+
+
+@pytest.mark.gpu
+def test_interleaved_large_matches_split():
+    from paper_1401_6235_b200 import interleaved as IL
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import workloads as W
+
+    n = (1 << 22) + 1
+    ps = W.PlaneSet("config2", n, torch.float64, 0)
+    for name in ("vtadd2", "vtdiv2", "vtsqrt1"):
+        planes = ps.planes(name)
+        out = K.empty_twofold(n, torch.float64)
+        K.KERNELS[name].loop(*planes, *out)
+        x = IL.from_split(K.TwofoldArray(planes[0], planes[1]))
+        args = (x,) if name == "vtsqrt1" else (x, IL.from_split(K.TwofoldArray(planes[2], planes[3])))
+        po = IL.empty_pairs(n)
+        IL.KERNELS[name](*args, po)
+        assert torch.equal(po[:, 0], out.value) and torch.equal(po[:, 1], out.error)
+
+
+def test_interleaved_validation_without_gpu():
+    from paper_1401_6235_b200 import interleaved as IL
+
+    x = torch.zeros((8, 2), dtype=torch.float64)
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        IL.vtadd2(x, x, x)
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        IL.vtadd2(np.zeros((8, 2)), x, x)
