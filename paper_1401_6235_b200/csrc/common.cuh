@@ -111,6 +111,77 @@ __device__ __forceinline__ void set_lane<float>(float4& v, int j, float x) {
   if (j == 0) v.x = x; else if (j == 1) v.y = x; else if (j == 2) v.z = x; else v.w = x;
 }
 
+// 32-byte vector (sm_100 256-bit LDG/STG: LDG.E.*.256 / STG.E.*.256)
+template <class T>
+struct alignas(32) Vec32 {
+  static constexpr int N = 32 / sizeof(T);
+  T v[N];
+};
+__device__ __forceinline__ Vec32<double> ld_stream(const Vec32<double>* p) {
+  Vec32<double> r;
+  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3])
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Vec32<float> ld_stream(const Vec32<float>* p) {
+  Vec32<float> r;
+  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3]), "=f"(r.v[4]), "=f"(r.v[5]),
+        "=f"(r.v[6]), "=f"(r.v[7])
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(Vec32<double>* p, const Vec32<double>& r) {
+  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]),
+               "d"(r.v[2]), "d"(r.v[3])
+               : "memory");
+}
+__device__ __forceinline__ void st_stream(Vec32<float>* p, const Vec32<float>& r) {
+  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
+               "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]),
+               "f"(r.v[7])
+               : "memory");
+}
+// 16-byte array vector (same LDG.128/STG.128 as double2/float4, indexable)
+template <class T>
+struct alignas(16) Vec16A {
+  static constexpr int N = 16 / sizeof(T);
+  T v[N];
+};
+__device__ __forceinline__ Vec16A<double> ld_stream(const Vec16A<double>* p) {
+  Vec16A<double> r;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Vec16A<float> ld_stream(const Vec16A<float>* p) {
+  Vec16A<float> r;
+  asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+      : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(Vec16A<double>* p, const Vec16A<double>& r) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]) : "memory");
+}
+__device__ __forceinline__ void st_stream(Vec16A<float>* p, const Vec16A<float>& r) {
+  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]),
+               "f"(r.v[2]), "f"(r.v[3])
+               : "memory");
+}
+template <class T, int VB>
+struct VecSel {
+  using type = Vec32<T>;
+};
+template <class T>
+struct VecSel<T, 16> {
+  using type = Vec16A<T>;
+};
+template <class T, int VB>
+using VecN = typename VecSel<T, VB>::type;
+
+inline bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31u) == 0; }
+
 // RAII device switch for host entry points that take a device ordinal
 struct DeviceGuard {
   int prev = -1;

@@ -16,6 +16,8 @@
 // the scalar grid-stride path (still one launch).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tf_math.cuh"
 
@@ -43,13 +45,13 @@ __device__ __forceinline__ void scalar_elem(const Planes<T>& p, int64_t i) {
   st_stream(p.out[1] + i, z.b);
 }
 
-template <class T, int OP>
+template <class T, int OP, int VB>
 __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t head,
                                                  int64_t nvec) {
   constexpr int NIN = OpInfo<OP>::NIN;
-  constexpr int E = Vec16<T>::N;
-  constexpr int U = Unroll<NIN>::U;
-  using V = typename Vec16<T>::type;
+  using V = VecN<T, VB>;
+  constexpr int E = V::N;
+  constexpr int U = (VB == 32) ? (NIN >= 3 ? 1 : 2) : Unroll<NIN>::U;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
 
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t
   const int64_t tail0 = head + nvec * E;
   for (int64_t i = tail0 + gtid; i < n; i += gstride) scalar_elem<T, OP>(p, i);
 
-  // 16-byte-vector body
+  // vector body: U steps of one VB-byte vector per plane, all loads first
   const V* vin[NIN];
 #pragma unroll
   for (int k = 0; k < NIN; k++) vin[k] = reinterpret_cast<const V*>(p.in[k] + head);
@@ -85,10 +87,10 @@ __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t
         for (int e = 0; e < E; e++) {
           T v[NIN];
 #pragma unroll
-          for (int k = 0; k < NIN; k++) v[k] = lane<T>(r[u][k], e);
+          for (int k = 0; k < NIN; k++) v[k] = r[u][k].v[e];
           P<T> z = apply<T, OP>(v);
-          set_lane<T>(o0, e, z.a);
-          set_lane<T>(o1, e, z.b);
+          o0.v[e] = z.a;
+          o1.v[e] = z.b;
         }
         st_stream(vo0 + j, o0);
         st_stream(vo1 + j, o1);
@@ -99,8 +101,6 @@ __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t
 
 // ---- dispatch ------------------------------------------------------------------
 
-using EwFn = void (*)(Planes<double>, int64_t, int64_t, int64_t);
-
 struct EwEntry {
   const void* fn;  // kernel symbol
   int nin;
@@ -108,26 +108,37 @@ struct EwEntry {
   int max_blocks_per_sm;  // occupancy, filled lazily
 };
 
-template <class T, int OP>
+template <class T, int OP, int VB>
 EwEntry make_entry() {
-  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP>), OpInfo<OP>::NIN,
-                 Unroll<OpInfo<OP>::NIN>::U, 0};
+  constexpr int NIN = OpInfo<OP>::NIN;
+  constexpr int U = (VB == 32) ? (NIN >= 3 ? 1 : 2) : Unroll<NIN>::U;
+  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>), NIN, U, 0};
 }
 
-template <class T, int... OPS>
+template <class T, int VB, int... OPS>
 struct Table {
   static EwEntry* get() {
-    static EwEntry t[] = {make_entry<T, OPS>()...};
+    static EwEntry t[] = {make_entry<T, OPS, VB>()...};
     return t;
   }
 };
 
-static EwEntry* table_for(int dtype) {
+#define TF_ALL_OPS 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21, 22, 23
+static EwEntry* table_for(int dtype, int vb) {
   if (dtype == TF_F64)
-    return Table<double, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20,
-                 21, 22, 23>::get();
-  return Table<float, 0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 17, 18, 19, 20, 21,
-               22, 23>::get();
+    return vb == 32 ? Table<double, 32, TF_ALL_OPS>::get() : Table<double, 16, TF_ALL_OPS>::get();
+  return vb == 32 ? Table<float, 32, TF_ALL_OPS>::get() : Table<float, 16, TF_ALL_OPS>::get();
+}
+
+// vector width of the split-layout body: 32-byte (sm_100 256-bit LDG/STG) by
+// default; TF_VEC_BYTES=16 selects the 128-bit variant (A/B measurements)
+static int vec_bytes() {
+  static int vb = 0;
+  if (!vb) {
+    const char* e = getenv("TF_VEC_BYTES");
+    vb = (e && atoi(e) == 16) ? 16 : 32;
+  }
+  return vb;
 }
 
 int ew_num_inputs(int op) {
@@ -144,20 +155,23 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     return fail(TF_EINVAL, "tf_elementwise: planes must be float32 or float64");
   if (n < 0) return fail(TF_EINVAL, "tf_elementwise: negative length");
   if (n == 0) return TF_OK;
-  EwEntry& ent = table_for(dtype)[op];
+  const int VBYTES = vec_bytes();
+  EwEntry& ent = table_for(dtype, VBYTES)[op];
   const size_t tsz = dtype == TF_F64 ? 8 : 4;
-  const int E = (int)(16 / tsz);
+  const int E = (int)(VBYTES / tsz);
   if (!in || !out || !out[0] || !out[1]) return fail(TF_EINVAL, "tf_elementwise: null plane");
   for (int k = 0; k < ent.nin; k++)
     if (!in[k]) return fail(TF_EINVAL, "tf_elementwise: null plane");
 
   // common misalignment -> scalar head, else all-scalar
-  uintptr_t mis = reinterpret_cast<uintptr_t>(out[0]) & 15u;
-  bool same = (mis % tsz) == 0 && (reinterpret_cast<uintptr_t>(out[1]) & 15u) == mis;
-  for (int k = 0; k < ent.nin; k++) same = same && (reinterpret_cast<uintptr_t>(in[k]) & 15u) == mis;
+  const uintptr_t amask = (uintptr_t)VBYTES - 1;
+  uintptr_t mis = reinterpret_cast<uintptr_t>(out[0]) & amask;
+  bool same = (mis % tsz) == 0 && (reinterpret_cast<uintptr_t>(out[1]) & amask) == mis;
+  for (int k = 0; k < ent.nin; k++)
+    same = same && (reinterpret_cast<uintptr_t>(in[k]) & amask) == mis;
   int64_t head, nvec;
   if (same) {
-    head = mis ? (int64_t)((16 - mis) / tsz) : 0;
+    head = mis ? (int64_t)((VBYTES - mis) / tsz) : 0;
     if (head > n) head = n;
     nvec = (n - head) / E;
   } else {

@@ -59,56 +59,54 @@ __global__ void __launch_bounds__(256) ew_il_kernel(ILArgs<T> p, int64_t n, int 
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   const int64_t nvec = vec ? n / E : 0;
 
-  for (int64_t j = gtid; j < nvec; j += gstride) {
-    // E elements: element e of step j is index j*E + e
-    T v[E][NIN];
-    if constexpr (AR == 22 || AR == 21 || AR == 2) {
-      const V* xa = reinterpret_cast<const V*>(p.a) + 2 * j;  // 2E scalars = E pairs
-      V r0 = ld_stream(xa), r1 = ld_stream(xa + 1);
+  // one step = E elements: a pair operand is one 32-byte vector (E pairs,
+  // sm_100 256-bit LDG), a plain plane one 16-byte vector; the result one
+  // 32-byte store.
+  using VP = Vec32<T>;   // E pairs
+  using VS = Vec16A<T>;  // E scalars
+  constexpr bool XP = (AR == 22 || AR == 21 || AR == 2);
+  constexpr int U = 2;  // steps in flight per thread: all loads issue before any math
+  for (int64_t base = gtid; base < nvec; base += gstride * U) {
+    VP xp[U], yp[U];
+    VS xs[U], ys[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * gstride;
+      if (j < nvec) {
+        if constexpr (XP) xp[u] = ld_stream(reinterpret_cast<const VP*>(p.a) + j);
+        else xs[u] = ld_stream(reinterpret_cast<const VS*>(p.a) + j);
+        if constexpr (AR == 22) yp[u] = ld_stream(reinterpret_cast<const VP*>(p.b) + j);
+        else if constexpr (AR == 21 || AR == 11) ys[u] = ld_stream(reinterpret_cast<const VS*>(p.b) + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * gstride;
+      if (j >= nvec) continue;
+      VP o;
 #pragma unroll
       for (int e = 0; e < E; e++) {
-        const V& r = (2 * e < E) ? r0 : r1;
-        v[e][0] = lane<T>(r, (2 * e) % E);
-        v[e][1] = lane<T>(r, (2 * e + 1) % E);
+        T v[NIN];
+        if constexpr (XP) {
+          v[0] = xp[u].v[2 * e];
+          v[1] = xp[u].v[2 * e + 1];
+        } else {
+          v[0] = xs[u].v[e];
+        }
+        if constexpr (AR == 22) {
+          v[2] = yp[u].v[2 * e];
+          v[3] = yp[u].v[2 * e + 1];
+        } else if constexpr (AR == 21) {
+          v[2] = ys[u].v[e];
+        } else if constexpr (AR == 11) {
+          v[1] = ys[u].v[e];
+        }
+        P<T> z = apply<T, OP>(v);
+        o.v[2 * e] = z.a;
+        o.v[2 * e + 1] = z.b;
       }
-    } else {
-      V r = ld_stream(reinterpret_cast<const V*>(p.a) + j);
-#pragma unroll
-      for (int e = 0; e < E; e++) v[e][0] = lane<T>(r, e);
+      st_stream(reinterpret_cast<VP*>(p.out) + j, o);
     }
-    if constexpr (AR == 22) {
-      const V* yb = reinterpret_cast<const V*>(p.b) + 2 * j;
-      V r0 = ld_stream(yb), r1 = ld_stream(yb + 1);
-#pragma unroll
-      for (int e = 0; e < E; e++) {
-        const V& r = (2 * e < E) ? r0 : r1;
-        v[e][2] = lane<T>(r, (2 * e) % E);
-        v[e][3] = lane<T>(r, (2 * e + 1) % E);
-      }
-    } else if constexpr (AR == 21) {
-      V r = ld_stream(reinterpret_cast<const V*>(p.b) + j);
-#pragma unroll
-      for (int e = 0; e < E; e++) v[e][2] = lane<T>(r, e);
-    } else if constexpr (AR == 11) {
-      V r = ld_stream(reinterpret_cast<const V*>(p.b) + j);
-#pragma unroll
-      for (int e = 0; e < E; e++) v[e][1] = lane<T>(r, e);
-    }
-    V o0, o1;
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-      P<T> z = apply<T, OP>(v[e]);
-      if (2 * e < E) {
-        set_lane<T>(o0, (2 * e) % E, z.a);
-        set_lane<T>(o0, (2 * e + 1) % E, z.b);
-      } else {
-        set_lane<T>(o1, (2 * e) % E, z.a);
-        set_lane<T>(o1, (2 * e + 1) % E, z.b);
-      }
-    }
-    V* o = reinterpret_cast<V*>(p.out) + 2 * j;
-    st_stream(o, o0);
-    st_stream(o + 1, o1);
   }
   // scalar remainder (or everything, when unaligned)
   for (int64_t i = nvec * E + gtid; i < n; i += gstride) {
@@ -229,11 +227,15 @@ int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* 
     if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_il: occupancy");
     ent.occ = o > 0 ? o : 1;
   }
-  int vec = aligned16(a) && aligned16(out) && (!binary || aligned16(b));
+  // pair arrays need 32-byte alignment, plain planes 16-byte
+  const int ar = nin_of[op] == 4 ? 22 : nin_of[op] == 3 ? 21 : op == TF_VTSQRT1 ? 2 : nin_of[op] == 2 ? 11 : 1;
+  const bool xpairs = ar == 22 || ar == 21 || ar == 2;
+  int vec = (xpairs ? aligned32(a) : aligned16(a)) && aligned32(out) &&
+            (!binary || (ar == 22 ? aligned32(b) : aligned16(b)));
   const int E = dtype == TF_F64 ? 2 : 4;
   ILArgs<double> p{static_cast<const double*>(a), static_cast<const double*>(b ? b : a),
                    static_cast<double*>(out)};
-  const int64_t blocks = grid_for(vec ? n / E : n, ent.occ);
+  const int64_t blocks = grid_for(vec ? (n / E + 1) / 2 : n, ent.occ);
   void* args[] = {&p, &n, &vec};
   return cuda_status(cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, s),
                      "tf_elementwise_il: launch");
