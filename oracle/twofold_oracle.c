@@ -332,6 +332,92 @@ int tfo_combine(int dtype, int g, const void* partials, const int64_t* counts,
 }
 
 /* ------------------------------------------------------------------------ */
+/* fused expression chains (demos.py:153-238), one instance per element       */
+
+#define DEFINE_FUSED(S, T)                                                     \
+  static int fused_##S(int fop, int64_t n, const T* const* in, T* const* out, int nt) { \
+    if (fop == 0 || fop == 1) {                                                \
+      _Pragma("omp parallel for schedule(static) num_threads(nt)")            \
+      for (int64_t i = 0; i < n; i++) {                                        \
+        pair_##S z;                                                            \
+        if (fop == 0) { /* tadd(tmul(a, x), y) */                              \
+          pair_##S m = tmul_##S(in[0][i], in[1][i], in[2][i], in[3][i]);       \
+          z = tadd_##S(m.a, m.b, in[4][i], in[5][i]);                          \
+        } else { /* tsub(c, tmul(a, b)) */                                     \
+          pair_##S m = tmul_##S(in[2][i], in[3][i], in[4][i], in[5][i]);       \
+          z = tsub_##S(in[0][i], in[1][i], m.a, m.b);                          \
+        }                                                                      \
+        out[0][i] = z.a; out[1][i] = z.b;                                      \
+      }                                                                        \
+      return 0;                                                                \
+    }                                                                          \
+    if (fop == 2) { /* demos.py:222-229 */                                     \
+      _Pragma("omp parallel for schedule(static) num_threads(nt)")            \
+      for (int64_t i = 0; i < n; i++) {                                        \
+        T a0 = in[0][i], a1 = in[1][i], b0 = in[2][i], b1 = in[3][i];          \
+        T c0 = in[4][i], c1 = in[5][i];                                        \
+        pair_##S bb = tmul_##S(b0, b1, b0, b1);                                \
+        pair_##S fa = tmul_##S((T)4, (T)0, a0, a1);                            \
+        pair_##S fac = tmul_##S(fa.a, fa.b, c0, c1);                           \
+        pair_##S disc = tsub_##S(bb.a, bb.b, fac.a, fac.b);                    \
+        pair_##S d = tsqrt_##S(disc.a, disc.b);                                \
+        T nb0 = -b0, nb1 = -b1;                                                \
+        pair_##S ta = tmul_##S((T)2, (T)0, a0, a1);                            \
+        pair_##S s0 = tsub_##S(nb0, nb1, d.a, d.b);                            \
+        pair_##S x0 = tdiv_##S(s0.a, s0.b, ta.a, ta.b);                        \
+        pair_##S s1 = tadd_##S(nb0, nb1, d.a, d.b);                            \
+        pair_##S x1 = tdiv_##S(s1.a, s1.b, ta.a, ta.b);                        \
+        out[0][i] = d.a; out[1][i] = d.b; out[2][i] = x0.a; out[3][i] = x0.b;  \
+        out[4][i] = x1.a; out[5][i] = x1.b;                                    \
+      }                                                                        \
+      return 0;                                                                \
+    }                                                                          \
+    if (fop == 3) { /* demos.py:175-192 */                                     \
+      _Pragma("omp parallel for schedule(static) num_threads(nt)")            \
+      for (int64_t s = 0; s < n; s++) {                                        \
+        pair_##S a[3][3], f[3], x[3];                                          \
+        for (int r = 0; r < 3; r++) {                                          \
+          for (int c = 0; c < 3; c++)                                          \
+            a[r][c] = mk_##S(in[0][(3 * r + c) * n + s], in[1][(3 * r + c) * n + s]); \
+          f[r] = mk_##S(in[2][r * n + s], in[3][r * n + s]);                   \
+        }                                                                      \
+        for (int k = 0; k < 3; k++)                                            \
+          for (int i = k + 1; i < 3; i++) {                                    \
+            pair_##S m = tdiv_##S(a[i][k].a, a[i][k].b, a[k][k].a, a[k][k].b); \
+            for (int j = k; j < 3; j++) {                                      \
+              pair_##S t = tmul_##S(m.a, m.b, a[k][j].a, a[k][j].b);           \
+              a[i][j] = tsub_##S(a[i][j].a, a[i][j].b, t.a, t.b);              \
+            }                                                                  \
+            pair_##S t = tmul_##S(m.a, m.b, f[k].a, f[k].b);                   \
+            f[i] = tsub_##S(f[i].a, f[i].b, t.a, t.b);                         \
+          }                                                                    \
+        for (int i = 2; i >= 0; i--) {                                         \
+          pair_##S acc = f[i];                                                 \
+          for (int j = i + 1; j < 3; j++) {                                    \
+            pair_##S t = tmul_##S(a[i][j].a, a[i][j].b, x[j].a, x[j].b);       \
+            acc = tsub_##S(acc.a, acc.b, t.a, t.b);                            \
+          }                                                                    \
+          x[i] = tdiv_##S(acc.a, acc.b, a[i][i].a, a[i][i].b);                 \
+        }                                                                      \
+        for (int r = 0; r < 3; r++) { out[0][r * n + s] = x[r].a; out[1][r * n + s] = x[r].b; } \
+      }                                                                        \
+      return 0;                                                                \
+    }                                                                          \
+    return -1;                                                                 \
+  }
+DEFINE_FUSED(d, double)
+DEFINE_FUSED(f, float)
+
+int tfo_fused(int fop, int dtype, int64_t n, const void* const* in, void* const* out,
+              int nthreads) {
+  if (n < 0) return -1;
+  int nt = clamp_threads(nthreads);
+  if (dtype == TF_F64) return fused_d(fop, n, (const double* const*)in, (double* const*)out, nt);
+  if (dtype == TF_F32) return fused_f(fop, n, (const float* const*)in, (float* const*)out, nt);
+  return -1;
+}
+
+/* ------------------------------------------------------------------------ */
 /* twofold Horner: r = (c_d, +0); r = _tadd1(_tmul1(r, x), c_k), k = d-1..0     */
 
 int tfo_horner(int dtype, int64_t n, const void* x_, const double* c, int degree,

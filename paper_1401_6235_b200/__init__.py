@@ -8,11 +8,12 @@ include/twofold_b200.h.  Adds twofold reductions, Horner and multi-GPU sharding.
 """
 
 from . import kernels  # noqa: F401
+from . import dist, fused, interleaved, reduce, workloads  # noqa: F401
 from .kernels import KERNELS, CoupledArray, KernelSpec, TwofoldArray, empty_twofold  # noqa: F401
 from .reduce import Twofold, vtdot, vthorner, vtsum, vtsum2  # noqa: F401
 
 __version__ = "0.1.0"
 
-__all__ = ["kernels", "KERNELS", "KernelSpec", "TwofoldArray", "CoupledArray",
+__all__ = ["kernels", "interleaved", "fused", "reduce", "dist", "workloads", "KERNELS", "KernelSpec", "TwofoldArray", "CoupledArray",
            "empty_twofold", "Twofold", "vtsum", "vtsum2", "vtdot", "vthorner",
            "__version__"]

@@ -1,0 +1,188 @@
+// fused.cu — fused twofold expression kernels.
+//
+// The reference chains scalar twofold ops in its application studies
+// (demos.py:153-199 Gauss elimination, demos.py:211-238 quadratic roots).  Run
+// over n independent instances, each chain becomes one data-parallel kernel
+// that keeps every intermediate in registers instead of a round trip through
+// HBM per op.  The op sequence and association order are the demos', op for op,
+// so results equal composing the elementwise kernels (and the reference) bit
+// for bit.
+//
+//   TF_FAXPY    z = tadd(tmul(a, x), y)                         6 in, 2 out planes
+//   TF_FSUBMUL  z = tsub(c, tmul(a, b))  (elimination update,   6 in, 2 out
+//               demos.py:182-184)
+//   TF_FQUAD    roots of a x^2 + b x + c (demos.py:222-229):    6 in, 6 out
+//               disc = tsub(tmul(b,b), tmul(tmul(4,a),c)); d = tsqrt(disc);
+//               x0 = tdiv(tsub(-b,d), tmul(2,a)); x1 = tdiv(tadd(-b,d), tmul(2,a))
+//   TF_FGAUSS3  naive 3x3 Gauss elimination + back substitution (demos.py:175-192)
+//               in: A value/error (9 planes each, row-major), f value/error (3);
+//               out: x value/error (3 planes each)
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "tf_math.cuh"
+
+namespace tf {
+
+template <class T>
+struct TF {
+  T a, b;
+};
+template <class T>
+__device__ __forceinline__ TF<T> mk(P<T> p) {
+  return {p.a, p.b};
+}
+template <class T>
+__device__ __forceinline__ TF<T> Tmul(TF<T> x, TF<T> y) {
+  return mk(tmul(x.a, x.b, y.a, y.b));
+}
+template <class T>
+__device__ __forceinline__ TF<T> Tadd(TF<T> x, TF<T> y) {
+  return mk(tadd(x.a, x.b, y.a, y.b));
+}
+template <class T>
+__device__ __forceinline__ TF<T> Tsub(TF<T> x, TF<T> y) {
+  return mk(tsub(x.a, x.b, y.a, y.b));
+}
+template <class T>
+__device__ __forceinline__ TF<T> Tdiv(TF<T> x, TF<T> y) {
+  return mk(tdiv(x.a, x.b, y.a, y.b));
+}
+template <class T>
+__device__ __forceinline__ TF<T> Tsqrt(TF<T> x) {
+  return mk(tsqrt(x.a, x.b));
+}
+
+template <class T>
+__device__ __forceinline__ TF<T> ld2(const T* v, const T* e, int64_t i) {
+  return {ld_stream(v + i), ld_stream(e + i)};
+}
+template <class T>
+__device__ __forceinline__ void st2(T* v, T* e, int64_t i, TF<T> z) {
+  st_stream(v + i, z.a);
+  st_stream(e + i, z.b);
+}
+
+struct FArgs {
+  const void* in[6];
+  void* out[6];
+};
+
+template <class T>
+__global__ void __launch_bounds__(256) axpy_kernel(FArgs p, int64_t n, int submul) {
+  const T* const* in = reinterpret_cast<const T* const*>(p.in);
+  T* const* out = reinterpret_cast<T* const*>(p.out);
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gstride) {
+    TF<T> a = ld2(in[0], in[1], i), x = ld2(in[2], in[3], i), y = ld2(in[4], in[5], i);
+    TF<T> z;
+    if (submul) z = Tsub(a, Tmul(x, y));  // a is c here: c - a*b
+    else z = Tadd(Tmul(a, x), y);
+    st2(out[0], out[1], i, z);
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) quad_kernel(FArgs p, int64_t n) {
+  const T* const* in = reinterpret_cast<const T* const*>(p.in);
+  T* const* out = reinterpret_cast<T* const*>(p.out);
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  const TF<T> four{T(4), T(0)}, two{T(2), T(0)};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gstride) {
+    TF<T> a = ld2(in[0], in[1], i), b = ld2(in[2], in[3], i), c = ld2(in[4], in[5], i);
+    TF<T> disc = Tsub(Tmul(b, b), Tmul(Tmul(four, a), c));
+    TF<T> d = Tsqrt(disc);
+    TF<T> nb{-b.a, -b.b};  // tneg (arith.py:838-842): exact sign flips
+    TF<T> two_a = Tmul(two, a);
+    TF<T> x0 = Tdiv(Tsub(nb, d), two_a);
+    TF<T> x1 = Tdiv(Tadd(nb, d), two_a);
+    st2(out[0], out[1], i, d);
+    st2(out[2], out[3], i, x0);
+    st2(out[4], out[5], i, x1);
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(128) gauss3_kernel(const T* __restrict__ Av,
+                                                     const T* __restrict__ Ae,
+                                                     const T* __restrict__ fv,
+                                                     const T* __restrict__ fe, T* __restrict__ xv,
+                                                     T* __restrict__ xe, int64_t n) {
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n; s += gstride) {
+    TF<T> a[3][3], f[3], x[3];
+#pragma unroll
+    for (int r = 0; r < 3; r++) {
+#pragma unroll
+      for (int c = 0; c < 3; c++) a[r][c] = ld2(Av + (3 * r + c) * n, Ae + (3 * r + c) * n, s);
+      f[r] = ld2(fv + r * n, fe + r * n, s);
+    }
+    // forward elimination, natural order, no pivoting (demos.py:177-185)
+#pragma unroll
+    for (int k = 0; k < 3; k++) {
+#pragma unroll
+      for (int i = k + 1; i < 3; i++) {
+        TF<T> m = Tdiv(a[i][k], a[k][k]);
+#pragma unroll
+        for (int j = k; j < 3; j++) a[i][j] = Tsub(a[i][j], Tmul(m, a[k][j]));
+        f[i] = Tsub(f[i], Tmul(m, f[k]));
+      }
+    }
+    // back substitution (demos.py:187-192)
+#pragma unroll
+    for (int i = 2; i >= 0; i--) {
+      TF<T> acc = f[i];
+#pragma unroll
+      for (int j = i + 1; j < 3; j++) acc = Tsub(acc, Tmul(a[i][j], x[j]));
+      x[i] = Tdiv(acc, a[i][i]);
+    }
+#pragma unroll
+    for (int r = 0; r < 3; r++) st2(xv + r * n, xe + r * n, s, x[r]);
+  }
+}
+
+int fused_launch(int fop, int dtype, int64_t n, const void* const* in, void* const* out,
+                 cudaStream_t s) {
+  if (fop < 0 || fop > 3) return fail(TF_EINVAL, "tf_fused: unknown fused op id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, "tf_fused: planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, "tf_fused: negative length");
+  if (n == 0) return TF_OK;
+  static const int nin[4] = {6, 6, 6, 4}, nout[4] = {2, 2, 6, 2};
+  if (!in || !out) return fail(TF_EINVAL, "tf_fused: null plane");
+  for (int k = 0; k < nin[fop]; k++)
+    if (!in[k]) return fail(TF_EINVAL, "tf_fused: null plane");
+  for (int k = 0; k < nout[fop]; k++)
+    if (!out[k]) return fail(TF_EINVAL, "tf_fused: null plane");
+  FArgs p{};
+  for (int k = 0; k < nin[fop]; k++) p.in[k] = in[k];
+  for (int k = 0; k < nout[fop]; k++) p.out[k] = out[k];
+  const int threads = fop == 3 ? 128 : 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  const int64_t cap = (int64_t)sm_count() * (fop == 3 ? 8 : 8);
+  blocks = blocks > cap ? cap : blocks;
+  const bool f64 = dtype == TF_F64;
+  switch (fop) {
+    case 0:
+    case 1:
+      if (f64) axpy_kernel<double><<<(unsigned)blocks, threads, 0, s>>>(p, n, fop);
+      else axpy_kernel<float><<<(unsigned)blocks, threads, 0, s>>>(p, n, fop);
+      break;
+    case 2:
+      if (f64) quad_kernel<double><<<(unsigned)blocks, threads, 0, s>>>(p, n);
+      else quad_kernel<float><<<(unsigned)blocks, threads, 0, s>>>(p, n);
+      break;
+    default:
+      if (f64)
+        gauss3_kernel<double><<<(unsigned)blocks, threads, 0, s>>>(
+            (const double*)in[0], (const double*)in[1], (const double*)in[2],
+            (const double*)in[3], (double*)out[0], (double*)out[1], n);
+      else
+        gauss3_kernel<float><<<(unsigned)blocks, threads, 0, s>>>(
+            (const float*)in[0], (const float*)in[1], (const float*)in[2], (const float*)in[3],
+            (float*)out[0], (float*)out[1], n);
+  }
+  return launch_status("tf_fused");
+}
+
+}  // namespace tf

@@ -392,8 +392,141 @@ def make_accumulate_kat():
     print("accumulate KAT:", kat)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "fused" not in sys.argv:
     make_elementwise()
     make_reductions()
     make_horner()
     make_accumulate_kat()
+
+
+# --------------------------------------------------------------------------
+# fused demo chains (demos.py:153-238) through the reference's scalar API
+
+
+def _ref_quadratic(a, b, c, fmt):
+    # demos.py:219-229, the same calls
+    four = twofold_from_decimal("4", fmt)
+    two = twofold_from_decimal("2", fmt)
+    disc = tf.tsub(tf.tmul(b, b), tf.tmul(tf.tmul(four, a), c))
+    d = tf.tsqrt(disc)
+    neg_b = tf.tneg(b)
+    two_a = tf.tmul(two, a)
+    x0 = tf.tdiv(tf.tsub(neg_b, d), two_a)
+    x1 = tf.tdiv(tf.tadd(neg_b, d), two_a)
+    return d, x0, x1
+
+
+def _ref_gauss3(a, f):
+    # demos.py:177-192, the same loops
+    a = [row[:] for row in a]
+    f = f[:]
+    for k in range(3):
+        for i in range(k + 1, 3):
+            m = tf.tdiv(a[i][k], a[k][k])
+            for j in range(k, 3):
+                a[i][j] = tf.tsub(a[i][j], tf.tmul(m, a[k][j]))
+            f[i] = tf.tsub(f[i], tf.tmul(m, f[k]))
+    x = [None, None, None]
+    for i in (2, 1, 0):
+        s = f[i]
+        for j in range(i + 1, 3):
+            s = tf.tsub(s, tf.tmul(a[i][j], x[j]))
+        x[i] = tf.tdiv(s, a[i][i])
+    return x
+
+
+def make_fused():
+    from twofold.demos import _CASES, _parse_c, gauss_solve, quadratic_roots
+
+    data, meta = {}, {}
+    for fmt, dtype in FMTS.items():
+        T = dtype
+        rng = np.random.default_rng(900 if fmt == "f64" else 901)
+        n = 512
+        tw = lambda v, e: tf.Twofold(T(v), T(e))  # noqa: E731
+        # axpy / submul on random twofolds
+        planes = [_planes(rng, n, dtype) for _ in range(3)]
+        flat = [p for pair in planes for p in pair]
+        ax0, ax1, sm0, sm1 = (np.empty(n, dtype) for _ in range(4))
+        for i in range(n):
+            a, x, y = (tw(planes[k][0][i], planes[k][1][i]) for k in range(3))
+            z = tf.tadd(tf.tmul(a, x), y)
+            ax0[i], ax1[i] = z
+            z = tf.tsub(a, tf.tmul(x, y))
+            sm0[i], sm1[i] = z
+        for k, p in enumerate(flat):
+            data["axpy/%s/in%d" % (fmt, k)] = p
+        data["axpy/%s/out" % fmt] = np.stack([ax0, ax1])
+        data["submul/%s/out" % fmt] = np.stack([sm0, sm1])
+        # quadratic: the demo's three cases, then random coefficients
+        cases = ["1e-8", "1+1e-8", "1-1e-8"]
+        A = [(T(1), T(0))] * len(cases)
+        B = [(T(2), T(0))] * len(cases)
+        C = [tuple(twofold_from_decimal(repr(_parse_c(c)), fmt)) for c in cases]
+        tokens = []
+        for c in cases:
+            rep = quadratic_roots(fmt, c).render()
+            tokens.append({ln.strip().split(": ")[0]: ln.strip().split(": ")[1]
+                           for ln in rep.splitlines() if ": " in ln and not ln.startswith("test")})
+        m = 509
+        a0 = rng.uniform(0.5, 2, m) * rng.choice([-1.0, 1.0], m)
+        b0 = rng.uniform(-4, 4, m)
+        c0 = rng.uniform(-1, 1, m)
+        A += [(T(v), T(v * 2.0**-30)) for v in a0]
+        B += [(T(v), T(-v * 2.0**-31)) for v in b0]
+        C += [(T(v), T(v * 2.0**-29)) for v in c0]
+        qin = [np.array([p[j] for p in P], dtype) for P in (A, B, C) for j in (0, 1)]
+        qout = [np.empty(len(A), dtype) for _ in range(6)]
+        for i in range(len(A)):
+            d, x0, x1 = _ref_quadratic(tf.Twofold(*A[i]), tf.Twofold(*B[i]), tf.Twofold(*C[i]), fmt)
+            for k, z in enumerate((d, x0, x1)):
+                qout[2 * k][i], qout[2 * k + 1][i] = z
+        for k in range(6):
+            data["quad/%s/in%d" % (fmt, k)] = qin[k]
+            data["quad/%s/out%d" % (fmt, k)] = qout[k]
+        meta["quad/%s" % fmt] = {"cases": cases, "tokens": tokens}
+        # gauss3: the demo's two systems, then random diagonally dominant ones
+        systems = []
+        for case in ("well3", "ill3"):
+            lam_t, f_t, _ = _CASES[case]
+            lam = twofold_from_decimal(lam_t, fmt)
+            one = twofold_from_decimal("1", fmt)
+            zero = twofold_from_decimal("0", fmt)
+            a = [[lam, one, zero], [zero, lam, one], [zero, zero, lam]]
+            f = [twofold_from_decimal(t, fmt) for t in f_t]
+            systems.append((a, f))
+        gtok = {}
+        for case in ("well3", "ill3"):
+            sol = gauss_solve(fmt, case).render().splitlines()[-1].split()
+            gtok[case] = sol
+        for _ in range(254):
+            M = rng.uniform(-1, 1, (3, 3)) + 4 * np.eye(3)
+            fv = rng.uniform(-5, 5, 3)
+            a = [[tw(M[r, c], M[r, c] * 2.0**-40) for c in range(3)] for r in range(3)]
+            f = [tw(fv[r], 0.0) for r in range(3)]
+            systems.append((a, f))
+        ns = len(systems)
+        Av = np.empty((3, 3, ns), dtype)
+        Ae = np.empty((3, 3, ns), dtype)
+        Fv = np.empty((3, ns), dtype)
+        Fe = np.empty((3, ns), dtype)
+        Xv = np.empty((3, ns), dtype)
+        Xe = np.empty((3, ns), dtype)
+        for s_, (a, f) in enumerate(systems):
+            for r in range(3):
+                for c in range(3):
+                    Av[r, c, s_], Ae[r, c, s_] = a[r][c]
+                Fv[r, s_], Fe[r, s_] = f[r]
+            x = _ref_gauss3(a, f)
+            for r in range(3):
+                Xv[r, s_], Xe[r, s_] = x[r]
+        for k, arr in (("Av", Av), ("Ae", Ae), ("Fv", Fv), ("Fe", Fe), ("Xv", Xv), ("Xe", Xe)):
+            data["gauss3/%s/%s" % (fmt, k)] = arr
+        meta["gauss3/%s" % fmt] = {"tokens": gtok}
+    np.savez_compressed(OUT / "fused.npz", **data)
+    (OUT / "fused.json").write_text(json.dumps(meta, indent=1))
+    print("fused fixtures written")
+
+
+if __name__ == "__main__" and "fused" in sys.argv:
+    make_fused()
