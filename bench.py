@@ -516,7 +516,7 @@ def run_elementwise(args, rank, world, local):
             "per_op": per_op,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches,
+            "gpu_launches": launches * world,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

@@ -23,7 +23,7 @@ for w in $what; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --csv \
         --log-file ${o}_launches.csv $cmd > ${o}_ncu_launches.log 2>&1; echo "rc=$?" >> ${o}_ncu_launches.log ;;
     ncu)
-      cmd="python bench.py --elems 33554432 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
+      cmd="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
       timeout 600 $cmd > ${o}_plain_full.log 2>&1 && \
       timeout 1200 ncu --set full --clock-control none --import-source on -k regex:ew_kernel -s 5 -c 5 \
         -o ${o}_prof_ew $cmd > ${o}_ncu_full.log 2>&1; echo "rc=$?" >> ${o}_ncu_full.log ;;

@@ -1,0 +1,60 @@
+"""Small launches of every kernel family for compute-sanitizer (memcheck /
+racecheck / initcheck / synccheck): odd sizes, misaligned views, partial
+tiles, multi-tile reductions with the last-CTA tree.  Exits non-zero on any
+mismatch against the oracle."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from oracle import oracle as o
+from paper_1401_6235_b200 import kernels as K, reduce as R, interleaved as IL, fused as F
+
+dev = "cuda:0"
+rng = np.random.default_rng(1)
+
+
+def put(a, off=0):
+    t = torch.empty(a.shape[0] + off, dtype=torch.float64 if a.dtype == np.float64 else torch.float32, device=dev)
+    t[off:].copy_(torch.from_numpy(a))
+    return t[off:]
+
+
+bad = 0
+for dt in (np.float64, np.float32):
+    for n in (1, 37, 4099):
+        for off in (0, 1):
+            for name in K.KERNELS:
+                spec = K.KERNELS[name]
+                nin = {"22": 4, "21": 3, "11": 2, "u2": 2, "u1": 1}[spec.arity]
+                ins = [rng.uniform(0.5, 2, n).astype(dt) for _ in range(nin)]
+                outs = [put(np.zeros(n, dt), off) for _ in range(2)]
+                spec.loop(*[put(a, off) for a in ins], *outs)
+                w = o.elementwise(name, *ins)
+                if not (np.array_equal(outs[0].cpu().numpy(), w[0]) and np.array_equal(outs[1].cpu().numpy(), w[1])):
+                    bad += 1
+                    print("mismatch", name, dt, n, off)
+    for n in (1, 5, 65536 * 3 + 7):
+        x = rng.uniform(-1, 1, n).astype(dt)
+        y = rng.uniform(-1, 1, n).astype(dt)
+        for rop in ("sum", "dot", "sum2"):
+            if rop == "sum":
+                z = R.vtsum(put(x))
+            elif rop == "dot":
+                z = R.vtdot(put(x), put(y))
+            else:
+                z = R.vtsum2((put(x), put(y)))
+            g = R.geometry(dt)
+            w = o.reduce(rop, x, None if rop == "sum" else y, geometry=g)
+            if (z.value, z.error) != (float(w[0]), float(w[1])):
+                bad += 1
+                print("reduce mismatch", rop, dt, n)
+    xs = rng.uniform(0.9, 1.1, 999).astype(dt)
+    out = K.empty_twofold(999, torch.float64 if dt == np.float64 else torch.float32)
+    R.vthorner(R.binomial_coeffs(20), put(xs), out)
+    p = IL.from_split(K.TwofoldArray(put(xs), put(xs)))
+    po = torch.empty_like(p)
+    IL.vtadd2(p, p, po)
+    F.vtaxpy(K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)))
+torch.cuda.synchronize()
+print("sanitize smoke done, mismatches:", bad)
+sys.exit(1 if bad else 0)
