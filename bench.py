@@ -599,7 +599,7 @@ def run_config4(args, rank, world, local):
                          "algorithmic_bytes": 16 * n, "peak_source": src},
             "e2e": {"value": world * 2 * n * args.e2e_steps / dt, "unit": "elem-ops/s",
                     "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 32},
-            "gpu_launches": K * (2 + (1 if world > 1 else 0)),
+            "gpu_launches": world * K * (2 + (1 if world > 1 else 0)),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -656,7 +656,7 @@ def run_config5(args, rank, world, local):
                          "frac": achieved / fp64_peak, "traffic": ncu_traffic("vthorner"),
                          "algorithmic_instr": instr,
                          "peak_source": "measured live: tf_fp64_peak (independent DFMA chains)"},
-            "gpu_launches": K,
+            "gpu_launches": world * K,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
