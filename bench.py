@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--elems", dest="n", type=int, default=0,
                     help="elements per GPU (default: the config's)")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
+                    help="replay each step as a CUDA graph (auto: n <= 2^22, launch-bound)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 25,
@@ -422,14 +424,38 @@ def run_elementwise(args, rank, world, local):
     torch.cuda.synchronize()
 
     K = args.steps
+    use_graph = args.graph == "on" or (args.graph == "auto" and n <= (1 << 22))
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in ops] for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per_op = {}
+    if use_graph:
+        # small, launch-bound steps: one CUDA graph per step, replayed K times
+        # (per-op times come from an eager pass with events around each launch)
+        for s in range(K):
+            for j, op in enumerate(ops):
+                ev[s][j][0].record(stream)
+                op.launch()
+                ev[s][j][1].record(stream)
+        torch.cuda.synchronize()
+        for j, op in enumerate(ops):
+            ts = [ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(K)]
+            per_op[op.name] = {"ms": sum(ts) / K, "eager": True}
+        g = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream()
+        with torch.cuda.graph(g, stream=cap):
+            for op in ops:
+                op.launch()
+        g.replay()
+        torch.cuda.synchronize()
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         start.record(stream)
         for s in range(K):
+            if use_graph:
+                g.replay()
+                continue
             for j, op in enumerate(ops):
                 ev[s][j][0].record(stream)
                 op.launch()
@@ -439,14 +465,18 @@ def run_elementwise(args, rank, world, local):
     barrier(world)
     elapsed_ms = max_over_ranks(start.elapsed_time(end), world)
     launches = K * len(ops)
-    log("timed region done: %.3f ms/step" % (elapsed_ms / K))
+    log("timed region done: %.3f ms/step (graph=%s)" % (elapsed_ms / K, use_graph))
 
-    per_op = {}
     for j, op in enumerate(ops):
-        ts = [ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(K)]
-        avg = sum(ts) / K
+        if use_graph:
+            avg = per_op[op.name]["ms"]
+            share = avg * K / elapsed_ms
+        else:
+            ts = [ev[s][j][0].elapsed_time(ev[s][j][1]) for s in range(K)]
+            avg = sum(ts) / K
+            share = sum(ts) / elapsed_ms
         per_op[op.name] = {"ms": avg, "gbs": op.nbytes / (avg * 1e-3) / 1e9,
-                           "bytes": op.nbytes, "share": sum(ts) / elapsed_ms}
+                           "bytes": op.nbytes, "share": share}
     dom = max(per_op, key=lambda k: per_op[k]["ms"])
     peak, peak_src = measured_peak()
     units_per_step = sum(op.units for op in ops)
@@ -507,6 +537,7 @@ def run_elementwise(args, rank, world, local):
             "dtype": "f64" if dtype == np.float64 else "f32",
             "data": "synthetic (seeded, device-generated with BASELINE distributions)",
             "config": {"workload": wl["desc"], "n_per_gpu": n, "ops": wl["names"],
+                       "timing": "cuda-graph replay per step" if use_graph else "eager launches",
                        "layout": "split SoA planes", "l2": "inputs %d MiB per plane >> 126 MB L2; no flush"
                        % (n * esz >> 20)},
             "hbm_gbs": world * bytes_per_step * K / (elapsed_ms * 1e-3) / 1e9,
