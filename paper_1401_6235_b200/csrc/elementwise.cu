@@ -68,32 +68,42 @@ __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t
   V* vo0 = reinterpret_cast<V*>(p.out[0] + head);
   V* vo1 = reinterpret_cast<V*>(p.out[1] + head);
 
-  for (int64_t base = gtid; base < nvec; base += gstride * U) {
-    V r[U][NIN];
+  // CTA-chunked: chunk c = vectors [c*CH, (c+1)*CH), CH = 256*U*R; thread t
+  // takes t, t+256, ... (coalesced).  With one CTA per chunk the hardware block
+  // scheduler balances SMs dynamically (no tail of idle SMs); a capped grid
+  // strides over chunks.
+  constexpr int R = 4;
+  constexpr int64_t CH = 256LL * U * R;
+  for (int64_t cb = (int64_t)blockIdx.x * CH; cb < nvec; cb += (int64_t)gridDim.x * CH) {
+#pragma unroll 1
+    for (int rr = 0; rr < R; rr++) {
+      const int64_t base = cb + (int64_t)rr * 256 * U + threadIdx.x;
+      V r[U][NIN];
 #pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int64_t j = base + u * gstride;
-      if (j < nvec) {
+      for (int u = 0; u < U; u++) {
+        const int64_t j = base + u * 256;
+        if (j < nvec) {
 #pragma unroll
-        for (int k = 0; k < NIN; k++) r[u][k] = ld_stream(vin[k] + j);
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-      const int64_t j = base + u * gstride;
-      if (j < nvec) {
-        V o0, o1;
-#pragma unroll
-        for (int e = 0; e < E; e++) {
-          T v[NIN];
-#pragma unroll
-          for (int k = 0; k < NIN; k++) v[k] = r[u][k].v[e];
-          P<T> z = apply<T, OP>(v);
-          o0.v[e] = z.a;
-          o1.v[e] = z.b;
+          for (int k = 0; k < NIN; k++) r[u][k] = ld_stream(vin[k] + j);
         }
-        st_stream(vo0 + j, o0);
-        st_stream(vo1 + j, o1);
+      }
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int64_t j = base + u * 256;
+        if (j < nvec) {
+          V o0, o1;
+#pragma unroll
+          for (int e = 0; e < E; e++) {
+            T v[NIN];
+#pragma unroll
+            for (int k = 0; k < NIN; k++) v[k] = r[u][k].v[e];
+            P<T> z = apply<T, OP>(v);
+            o0.v[e] = z.a;
+            o1.v[e] = z.b;
+          }
+          st_stream(vo0 + j, o0);
+          st_stream(vo1 + j, o1);
+        }
       }
     }
   }
@@ -185,9 +195,17 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     if (e != cudaSuccess) return cuda_status(e, "tf_elementwise: occupancy");
     ent.max_blocks_per_sm = b > 0 ? b : 1;
   }
-  const int64_t work = nvec > 0 ? (nvec + ent.unroll - 1) / ent.unroll : n;
-  int64_t blocks = (work + 255) / 256;
-  const int64_t cap = (int64_t)sm_count() * ent.max_blocks_per_sm;
+  // one CTA per chunk of 256*U*4 vectors (hardware-balanced); TF_EW_SCHED=
+  // persistent caps the grid at the resident CTAs instead (A/B measurements)
+  const int64_t chunk = 256LL * ent.unroll * 4;
+  int64_t blocks = nvec > 0 ? (nvec + chunk - 1) / chunk : (n + 255) / 256;
+  const int64_t resident = (int64_t)sm_count() * ent.max_blocks_per_sm;
+  static int persistent = -1;
+  if (persistent < 0) {
+    const char* e = getenv("TF_EW_SCHED");
+    persistent = (e && e[0] == 'p') ? 1 : 0;
+  }
+  const int64_t cap = persistent || nvec == 0 ? resident : (int64_t)0x7fffffff;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
 
