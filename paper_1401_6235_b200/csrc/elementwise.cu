@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(256) dotted_vec_kernel(const typename Vec16<T>
 template <class T, int BASE>
 static int dotted_t(int64_t n, const void* x, const void* y, void* r, cudaStream_t s) {
   constexpr int E = Vec16<T>::N;
-  const int64_t cap = (int64_t)sm_count() * 8;
+  const int64_t cap = 0x7fffffffLL;  // one CTA per chunk: hardware-balanced
   const bool vec = aligned16(x) && aligned16(r) && (BASE > 2 || aligned16(y)) && n % E == 0;
   if (vec) {
     int64_t nvec = n / E;

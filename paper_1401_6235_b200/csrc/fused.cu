@@ -159,8 +159,7 @@ int fused_launch(int fop, int dtype, int64_t n, const void* const* in, void* con
   for (int k = 0; k < nout[fop]; k++) p.out[k] = out[k];
   const int threads = fop == 3 ? 128 : 256;
   int64_t blocks = (n + threads - 1) / threads;
-  const int64_t cap = (int64_t)sm_count() * (fop == 3 ? 8 : 8);
-  blocks = blocks > cap ? cap : blocks;
+  blocks = blocks > 0x7fffffffLL ? 0x7fffffffLL : blocks;  // one CTA per chunk
   const bool f64 = dtype == TF_F64;
   switch (fop) {
     case 0:

@@ -76,18 +76,9 @@ static int horner_t(int64_t n, const void* x, const double* coeffs, int degree, 
   for (int k = 0; k <= degree; k++) c.c[k] = (T)coeffs[k];
   for (int k = degree + 1; k <= TF_HORNER_MAX_DEGREE; k++) c.c[k] = T(0);
   constexpr int ILP = 4;
-  static int occ[2] = {0, 0};
-  const void* fn = degree == 20 ? (const void*)&horner_kernel<T, ILP, 20>
-                                : (const void*)&horner_kernel<T, ILP, -1>;
-  int& o = occ[degree == 20 ? 0 : 1];
-  if (!o) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fn, 256, 0);
-    if (e != cudaSuccess) return cuda_status(e, "tf_horner: occupancy");
-    if (o < 1) o = 1;
-  }
   int64_t blocks = (n + 256 * ILP - 1) / (256 * ILP);
-  const int64_t cap = (int64_t)sm_count() * o;
-  blocks = blocks > cap ? cap : (blocks < 1 ? 1 : blocks);
+  // one CTA per 256*ILP points (hardware-balanced, no idle-SM tail)
+  blocks = blocks > 0x7fffffffLL ? 0x7fffffffLL : (blocks < 1 ? 1 : blocks);
   const T* px = static_cast<const T*>(x);
   T* p0 = static_cast<T*>(o0);
   T* p1 = static_cast<T*>(o1);
