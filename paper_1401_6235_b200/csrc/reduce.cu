@@ -22,6 +22,8 @@
 // per input plane.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tf_math.cuh"
 
@@ -123,6 +125,71 @@ __device__ __forceinline__ P<T> cta_tree(P<T> acc, int have, int* have_out) {
   return acc;
 }
 
+// partial tile or unaligned planes: the canonical order, scalar loads, bounds checked
+template <class T, int ROP>
+__device__ __forceinline__ void fold_scalar(const T* a, const T* b, int64_t n, int64_t base,
+                                            P<T>& acc, int& have) {
+  constexpr int V = Geo<T>::V;
+  const int w = threadIdx.x;
+  for (int k = 0; k < RK; k++) {
+    for (int e = 0; e < V; e++) {
+      const int64_t i = base + (int64_t)V * (w + (int64_t)RW * k) + e;
+      if (i >= n) continue;
+      T x = ld_stream(a + i);
+      T y = (ROP == TF_RSUM) ? x : ld_stream(b + i);
+      if (!have) {
+        acc = first_term<T, ROP>(x, y);
+        have = 1;
+      } else {
+        acc = fold<T, ROP>(acc, x, y);
+      }
+    }
+  }
+}
+
+// lane tree -> tile partial; the last CTA (atomic ticket) runs the tile tree
+template <class T>
+__device__ __forceinline__ void finish_tile(P<T> acc, int have, int64_t t, int64_t ntiles,
+                                            P<T>* tiles, unsigned* counter, T* out) {
+  int h;
+  acc = cta_tree(acc, have, &h);
+
+  __shared__ int is_last;
+  if (threadIdx.x == 0) {
+    tiles[t].a = acc.a;
+    tiles[t].b = acc.b;
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    is_last = (prev == (unsigned)(ntiles - 1));
+  }
+  __syncthreads();
+  if (!is_last) return;
+  __threadfence();
+
+  // last CTA: the tile tree.  Thread j owns the aligned block of B2 tiles
+  // [j*B2, (j+1)*B2); blocks are complete subtrees, so block trees followed by
+  // the CTA tree reproduce the global adjacent-pair tree exactly.
+  int64_t per = (ntiles + RW - 1) / RW;
+  int64_t B2 = 1;
+  while (B2 < per) B2 <<= 1;
+  const int64_t lo = (int64_t)threadIdx.x * B2;
+  const int64_t hi = lo + B2 < ntiles ? lo + B2 : ntiles;
+  P<T> part{T(0), T(0)};
+  int ph = 0;
+  if (lo < ntiles) {
+    part = block_tree(tiles, lo, hi);
+    ph = 1;
+  }
+  __syncthreads();  // shared scratch of cta_tree is reused
+  part = cta_tree(part, ph, &h);
+  if (threadIdx.x == 0) {
+    out[0] = part.a;
+    out[1] = part.b;
+    *counter = 0u;  // leave the workspace ready for the next call
+  }
+}
+
+// ---- variant 1: register path (LDG.128 batches) --------------------------------
 template <class T, int ROP, bool VEC>
 __global__ void __launch_bounds__(RW) reduce_kernel(const T* __restrict__ a,
                                                     const T* __restrict__ b, int64_t n,
@@ -162,59 +229,118 @@ __global__ void __launch_bounds__(RW) reduce_kernel(const T* __restrict__ a,
     }
     have = 1;
   } else {
-    // partial tile or unaligned planes: same order, scalar loads, bounds checked
-    for (int k = 0; k < RK; k++) {
-      for (int e = 0; e < V; e++) {
-        const int64_t i = base + (int64_t)V * (w + (int64_t)RW * k) + e;
-        if (i >= n) continue;
-        T x = ld_stream(a + i);
-        T y = (ROP == TF_RSUM) ? x : ld_stream(b + i);
-        if (!have) {
-          acc = first_term<T, ROP>(x, y);
-          have = 1;
-        } else {
-          acc = fold<T, ROP>(acc, x, y);
+    fold_scalar<T, ROP>(a, b, n, base, acc, have);
+  }
+  finish_tile(acc, have, t, ntiles, tiles, counter, out);
+}
+
+// ---- variant 2: TMA bulk-copy path (cp.async.bulk -> smem ring, mbarriers) ------
+// A tile is streamed through shared memory in stages of KS k-steps (KS*4 KB per
+// plane): one elected thread arms an mbarrier with the byte count and issues
+// one bulk copy per plane (UBLKCP); lanes read their 16-byte vectors back from
+// shared memory in exactly the canonical order (bank-conflict free: lane w reads
+// bytes [16w, 16w+16) of each 4 KB k-row).  NST stages in flight per CTA, two
+// CTAs per SM.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int ROP>
+struct BulkGeo {
+  static constexpr int NPL = ROP == TF_RSUM ? 1 : 2;  // planes
+  static constexpr int KS = ROP == TF_RSUM ? 8 : 4;   // k-steps per stage
+  static constexpr int NST = 3;                        // stages in flight
+  static constexpr int STAGE = RW * 16 * KS;           // bytes per plane per stage
+  static constexpr int SMEM = NST * NPL * STAGE;       // 96 KB: two CTAs per SM
+};
+
+template <class T, int ROP>
+__global__ void __launch_bounds__(RW) reduce_bulk_kernel(const T* __restrict__ a,
+                                                         const T* __restrict__ b, int64_t n,
+                                                         int64_t ntiles, P<T>* tiles,
+                                                         unsigned* counter, T* out) {
+  using G = BulkGeo<ROP>;
+  constexpr int V = Geo<T>::V;
+  constexpr int64_t L = Geo<T>::L;
+  constexpr int NSTAGES = RK / G::KS;
+  using Vt = typename Vec16<T>::type;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[G::NST];
+  const int w = threadIdx.x;
+  const int64_t t = blockIdx.x;
+  const int64_t base = t * L;
+  P<T> acc{T(0), T(0)};
+  int have = 0;
+
+  if (base + L <= n) {
+    const T* planes[2] = {a + base, (ROP == TF_RSUM ? a : b) + base};
+    if (w == 0) {
+      for (int q = 0; q < G::NST; q++) mbar_init(&bar[q], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    auto issue = [&](int stage, int buf) {
+      mbar_expect_tx(&bar[buf], G::NPL * G::STAGE);
+#pragma unroll
+      for (int pl = 0; pl < G::NPL; pl++)
+        bulk_g2s(smem + (buf * G::NPL + pl) * G::STAGE,
+                 planes[pl] + (int64_t)stage * G::KS * RW * V, G::STAGE, &bar[buf]);
+    };
+    if (w == 0)
+      for (int q = 0; q < G::NST && q < NSTAGES; q++) issue(q, q);
+#pragma unroll 1
+    for (int j = 0; j < NSTAGES; j++) {
+      const int buf = j % G::NST;
+      mbar_wait(&bar[buf], (uint32_t)((j / G::NST) & 1));
+      const Vt* sa = reinterpret_cast<const Vt*>(smem + (buf * G::NPL) * G::STAGE) + w;
+      const Vt* sb = reinterpret_cast<const Vt*>(smem + (buf * G::NPL + G::NPL - 1) * G::STAGE) + w;
+#pragma unroll
+      for (int kl = 0; kl < G::KS; kl++) {
+        Vt ra = sa[kl * RW];
+        Vt rb = ROP == TF_RSUM ? ra : sb[kl * RW];
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          T x = lane<T>(ra, e);
+          T y = (ROP == TF_RSUM) ? x : lane<T>(rb, e);
+          if (j == 0 && kl == 0 && e == 0) acc = first_term<T, ROP>(x, y);
+          else acc = fold<T, ROP>(acc, x, y);
         }
       }
+      __syncthreads();  // every lane is done with this buffer
+      if (w == 0 && j + G::NST < NSTAGES) issue(j + G::NST, buf);
     }
+    have = 1;
+  } else {
+    fold_scalar<T, ROP>(a, b, n, base, acc, have);
   }
-
-  int h;
-  acc = cta_tree(acc, have, &h);
-
-  __shared__ int is_last;
-  if (threadIdx.x == 0) {
-    tiles[t].a = acc.a;
-    tiles[t].b = acc.b;
-    __threadfence();
-    unsigned prev = atomicAdd(counter, 1u);
-    is_last = (prev == (unsigned)(ntiles - 1));
-  }
-  __syncthreads();
-  if (!is_last) return;
-  __threadfence();
-
-  // last CTA: the tile tree.  Thread j owns the aligned block of B2 tiles
-  // [j*B2, (j+1)*B2); blocks are complete subtrees, so block trees followed by
-  // the CTA tree reproduce the global adjacent-pair tree exactly.
-  int64_t per = (ntiles + RW - 1) / RW;
-  int64_t B2 = 1;
-  while (B2 < per) B2 <<= 1;
-  const int64_t lo = (int64_t)threadIdx.x * B2;
-  const int64_t hi = lo + B2 < ntiles ? lo + B2 : ntiles;
-  P<T> part{T(0), T(0)};
-  int ph = 0;
-  if (lo < ntiles) {
-    part = block_tree(tiles, lo, hi);
-    ph = 1;
-  }
-  __syncthreads();  // shared scratch of cta_tree is reused
-  part = cta_tree(part, ph, &h);
-  if (threadIdx.x == 0) {
-    out[0] = part.a;
-    out[1] = part.b;
-    *counter = 0u;  // leave the workspace ready for the next call
-  }
+  finish_tile(acc, have, t, ntiles, tiles, counter, out);
 }
 
 struct ShardIdx {
@@ -273,6 +399,17 @@ int reduce_geometry(int dtype, int* V, int* W, int* K) {
   return TF_OK;
 }
 
+// TF_REDUCE_PATH=ldg selects the register path for A/B runs; default is the
+// TMA bulk-copy path whenever the planes are 16-byte aligned
+static bool use_bulk() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("TF_REDUCE_PATH");
+    v = (e && e[0] == 'l') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <class T, int ROP>
 static int reduce_t(int64_t n, const void* a, const void* b, void* out, void* ws,
                     cudaStream_t s) {
@@ -282,12 +419,23 @@ static int reduce_t(int64_t n, const void* a, const void* b, void* out, void* ws
   const bool vec = aligned16(a) && (ROP == TF_RSUM || aligned16(b));
   const T* pa = static_cast<const T*>(a);
   const T* pb = static_cast<const T*>(b ? b : a);
-  if (vec)
-    reduce_kernel<T, ROP, true><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
-                                                            static_cast<T*>(out));
-  else
-    reduce_kernel<T, ROP, false><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
-                                                             static_cast<T*>(out));
+  T* po = static_cast<T*>(out);
+  if (vec && use_bulk()) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(reduce_bulk_kernel<T, ROP>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           BulkGeo<ROP>::SMEM);
+      if (e != cudaSuccess) return cuda_status(e, "tf_reduce: smem attribute");
+      attr = true;
+    }
+    reduce_bulk_kernel<T, ROP><<<(unsigned)nt, RW, BulkGeo<ROP>::SMEM, s>>>(pa, pb, n, nt, tiles,
+                                                                           counter, po);
+  } else if (vec) {
+    reduce_kernel<T, ROP, true><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter, po);
+  } else {
+    reduce_kernel<T, ROP, false><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter, po);
+  }
   return launch_status("tf_reduce");
 }
 
