@@ -399,13 +399,14 @@ int reduce_geometry(int dtype, int* V, int* W, int* K) {
   return TF_OK;
 }
 
-// TF_REDUCE_PATH=ldg selects the register path for A/B runs; default is the
-// TMA bulk-copy path whenever the planes are 16-byte aligned
+// Both full-tile paths sit at the read-bandwidth wall (config 4, n=2^30:
+// register path 7256 GB/s, bulk path 7191 GB/s); the register path is the
+// default, TF_REDUCE_PATH=bulk selects the TMA bulk-copy path.
 static bool use_bulk() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("TF_REDUCE_PATH");
-    v = (e && e[0] == 'l') ? 0 : 1;
+    v = (e && e[0] == 'b') ? 1 : 0;
   }
   return v == 1;
 }
