@@ -1,0 +1,27 @@
+"""Every selectable kernel variant is parity-checked: the A/B switches
+(TF_VEC_BYTES=16, TF_EW_SCHED=persistent, TF_REDUCE_PATH=bulk) are read once per
+process, so each runs tools/sanitize_smoke.py (all kernel families, odd sizes,
+misaligned views, partial tiles, vs the oracle) in its own subprocess."""
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+
+VARIANTS = [{}, {"TF_VEC_BYTES": "16"}, {"TF_EW_SCHED": "persistent"},
+            {"TF_REDUCE_PATH": "bulk"}, {"TF_HOST_SLOTS": "2", "TF_HOST_CHUNK_MB": "1"}]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env", VARIANTS, ids=lambda e: ",".join("%s=%s" % kv for kv in e.items()) or "default")
+def test_variant_parity(env):
+    e = dict(os.environ)
+    e.update(env)
+    r = subprocess.run([sys.executable, str(ROOT / "tools" / "sanitize_smoke.py")], env=e,
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "mismatches: 0" in r.stdout

@@ -55,6 +55,16 @@ for dt in (np.float64, np.float32):
     po = torch.empty_like(p)
     IL.vtadd2(p, p, po)
     F.vtaxpy(K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)))
+# host-plane pipeline (pinned and pageable), several chunks
+for dt in (np.float64, np.float32):
+    n = 3 * (1 << 18) + 5
+    ins = [rng.uniform(0.5, 2, n).astype(dt) for _ in range(4)]
+    out = K.empty_twofold(n, dt, device="cpu")
+    K.vtdiv2(K.TwofoldArray(ins[0], ins[1]), K.TwofoldArray(ins[2], ins[3]), out)
+    w = o.elementwise("vtdiv2", *ins)
+    if not (np.array_equal(out.value, w[0]) and np.array_equal(out.error, w[1])):
+        bad += 1
+        print("host path mismatch", dt)
 torch.cuda.synchronize()
 print("sanitize smoke done, mismatches:", bad)
 sys.exit(1 if bad else 0)
