@@ -124,8 +124,8 @@ struct HostPipe {
   bool ready = false;
   cudaStream_t st[MAX_SLOTS] = {};
   cudaEvent_t done[MAX_SLOTS] = {};
-  void* dbuf[MAX_SLOTS][6] = {};  // device: 4 inputs + 2 outputs
-  void* hbuf[MAX_SLOTS][6] = {};  // pinned staging for pageable planes (lazy)
+  std::vector<void*> dbuf[MAX_SLOTS];  // device staging planes (grown on demand)
+  std::vector<void*> hbuf[MAX_SLOTS];  // pinned staging for pageable planes (lazy)
   CopyPool* pool = nullptr;
 };
 static HostPipe g_pipe[64];
@@ -144,23 +144,27 @@ static int pipe_init(HostPipe& p) {
     cudaError_t e = cudaStreamCreateWithFlags(&p.st[s], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.done[s], cudaEventDisableTiming);
     if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: stream");
-    for (int k = 0; k < 6; k++) {
-      e = cudaMalloc(&p.dbuf[s][k], p.chunk_bytes);
-      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: staging alloc");
-    }
   }
   p.ready = true;
   return TF_OK;
 }
 
-static int ensure_host_staging(HostPipe& p) {
-  if (p.hbuf[0][0]) return TF_OK;
-  for (int s = 0; s < p.slots; s++)
-    for (int k = 0; k < 6; k++) {
-      cudaError_t e = cudaHostAlloc(&p.hbuf[s][k], p.chunk_bytes, cudaHostAllocPortable);
-      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: pinned staging alloc");
+static int ensure_planes(HostPipe& p, int planes, bool pinned_staging) {
+  for (int s = 0; s < p.slots; s++) {
+    while ((int)p.dbuf[s].size() < planes) {
+      void* d = nullptr;
+      cudaError_t e = cudaMalloc(&d, p.chunk_bytes);
+      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: staging alloc");
+      p.dbuf[s].push_back(d);
     }
-  if (!p.pool) {
+    while (pinned_staging && (int)p.hbuf[s].size() < planes) {
+      void* h = nullptr;
+      cudaError_t e = cudaHostAlloc(&h, p.chunk_bytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: pinned staging alloc");
+      p.hbuf[s].push_back(h);
+    }
+  }
+  if (pinned_staging && !p.pool) {
     unsigned hw = std::thread::hardware_concurrency();
     int nt = hw ? (int)hw : 4;
     if (const char* v = getenv("TF_HOST_THREADS")) nt = atoi(v) > 0 ? atoi(v) : nt;
@@ -179,51 +183,80 @@ static bool is_pinned(const void* ptr) {
   return a.type == cudaMemoryTypeHost;
 }
 
-}  // namespace tf
-
-using namespace tf;
-
-extern "C" int tf_elementwise_host(int op, int dtype, int64_t n, const void* const* in,
-                                   void* const* out, int device) {
-  const int nin = ew_num_inputs(op);
-  if (nin < 0) return fail(TF_EINVAL, "tf_elementwise_host: unknown op id");
+// Run `nops` ops over the same n elements of host planes in one pipelined pass.
+// Distinct input planes (by address) cross the host link once per chunk however
+// many ops read them; every op's two outputs come back, in op order.
+static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void* const* in,
+                      void* const* out, int device, const char* who) {
+  if (nops < 1 || nops > 64) return fail(TF_EINVAL, std::string(who) + ": 1..64 ops per batch");
   if (dtype != TF_F32 && dtype != TF_F64)
-    return fail(TF_EINVAL, "tf_elementwise_host: planes must be float32 or float64");
-  if (n < 0) return fail(TF_EINVAL, "tf_elementwise_host: negative length");
+    return fail(TF_EINVAL, std::string(who) + ": planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, std::string(who) + ": negative length");
+  if (!in || !out) return fail(TF_EINVAL, std::string(who) + ": null plane");
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  // distinct inputs; per op the index of each of its inputs among them
+  std::vector<const void*> uniq;
+  std::vector<int> idx((size_t)nops * 4, -1);
+  for (int o = 0; o < nops; o++) {
+    const int nin = ew_num_inputs(ops[o]);
+    if (nin < 0) return fail(TF_EINVAL, std::string(who) + ": unknown op id");
+    if (!out[2 * o] || !out[2 * o + 1]) return fail(TF_EINVAL, std::string(who) + ": null plane");
+    for (int k = 0; k < nin; k++) {
+      const void* ptr = in[4 * o + k];
+      if (!ptr) return fail(TF_EINVAL, std::string(who) + ": null plane");
+      int u = -1;
+      for (size_t q = 0; q < uniq.size(); q++)
+        if (uniq[q] == ptr) u = (int)q;
+      if (u < 0) {
+        u = (int)uniq.size();
+        uniq.push_back(ptr);
+      }
+      idx[4 * o + k] = u;
+    }
+  }
+  // no op may read what another op of the batch writes (no intra-batch chains)
+  const uintptr_t span = (uintptr_t)n * tsz;
+  for (int o = 0; o < 2 * nops; o++) {
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(out[o]);
+    for (const void* u : uniq) {
+      const uintptr_t b0 = reinterpret_cast<uintptr_t>(u);
+      if (n && a0 < b0 + span && b0 < a0 + span)
+        return fail(TF_EINVAL, std::string(who) + ": out must not alias an input");
+    }
+  }
   if (n == 0) return TF_OK;
-  if (!in || !out || !out[0] || !out[1]) return fail(TF_EINVAL, "tf_elementwise_host: null plane");
-  for (int k = 0; k < nin; k++)
-    if (!in[k]) return fail(TF_EINVAL, "tf_elementwise_host: null plane");
+
   DeviceGuard g(device);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return fail(TF_EINVAL, "tf_elementwise_host: device ordinal");
+  if (dev < 0 || dev >= 64) return fail(TF_EINVAL, std::string(who) + ": device ordinal");
   HostPipe& p = g_pipe[dev];
   std::lock_guard<std::mutex> lock(p.mu);
   int rc = pipe_init(p);
   if (rc) return rc;
 
-  bool pin_in[4] = {true, true, true, true}, pin_out[2];
+  const int U = (int)uniq.size();
+  const int NP = U + 2 * nops;  // staging planes per slot: inputs, then outputs
+  std::vector<char> pin_in(U), pin_out(2 * nops);
   bool any_pageable = false;
-  for (int k = 0; k < nin; k++) any_pageable |= !(pin_in[k] = is_pinned(in[k]));
-  for (int k = 0; k < 2; k++) any_pageable |= !(pin_out[k] = is_pinned(out[k]));
-  if (any_pageable && (rc = ensure_host_staging(p))) return rc;
+  for (int q = 0; q < U; q++) any_pageable |= !(pin_in[q] = is_pinned(uniq[q]));
+  for (int o = 0; o < 2 * nops; o++) any_pageable |= !(pin_out[o] = is_pinned(out[o]));
+  if ((rc = ensure_planes(p, NP, any_pageable))) return rc;
 
-  const size_t tsz = dtype == TF_F64 ? 8 : 4;
   const int64_t chunk = p.chunk_bytes / (int64_t)tsz;
   const int64_t nchunks = (n + chunk - 1) / chunk;
   const int S = p.slots;
   std::vector<int64_t> slot_off(S, -1);  // chunk offset in flight in each slot
 
-  auto finish = [&](int s) -> int {  // wait for slot s; unstage pageable outputs
+  auto finish = [&](int s) -> int {  // wait for slot s; unstage pageable outputs in op order
     if (slot_off[s] < 0) return TF_OK;
     cudaError_t e = cudaEventSynchronize(p.done[s]);
-    if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: sync");
+    if (e != cudaSuccess) return cuda_status(e, who);
     const int64_t off = slot_off[s];
     const int64_t m = (n - off) < chunk ? (n - off) : chunk;
-    for (int k = 0; k < 2; k++)
-      if (!pin_out[k])
-        par_memcpy(*p.pool, static_cast<char*>(out[k]) + off * tsz, p.hbuf[s][4 + k],
+    for (int o = 0; o < 2 * nops; o++)
+      if (!pin_out[o])
+        par_memcpy(*p.pool, static_cast<char*>(out[o]) + off * tsz, p.hbuf[s][U + o],
                    (size_t)m * tsz);
     slot_off[s] = -1;
     return TF_OK;
@@ -236,30 +269,53 @@ extern "C" int tf_elementwise_host(int op, int dtype, int64_t n, const void* con
     const int64_t m = (n - off) < chunk ? (n - off) : chunk;
     const size_t bytes = (size_t)m * tsz;
     cudaStream_t st = p.st[s];
-    const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
-    for (int k = 0; k < nin; k++) {
-      const void* src = static_cast<const char*>(in[k]) + off * tsz;
-      if (!pin_in[k]) {
-        par_memcpy(*p.pool, p.hbuf[s][k], src, bytes);
-        src = p.hbuf[s][k];
+    for (int q = 0; q < U; q++) {
+      const void* src = static_cast<const char*>(uniq[q]) + off * tsz;
+      if (!pin_in[q]) {
+        par_memcpy(*p.pool, p.hbuf[s][q], src, bytes);
+        src = p.hbuf[s][q];
       }
-      cudaError_t e = cudaMemcpyAsync(p.dbuf[s][k], src, bytes, cudaMemcpyHostToDevice, st);
-      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: H2D");
-      din[k] = p.dbuf[s][k];
+      cudaError_t e = cudaMemcpyAsync(p.dbuf[s][q], src, bytes, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_status(e, who);
     }
-    void* dout[2] = {p.dbuf[s][4], p.dbuf[s][5]};
-    if ((rc = ew_launch(op, dtype, m, din, dout, st))) return rc;
-    for (int k = 0; k < 2; k++) {
-      void* dst = pin_out[k] ? static_cast<char*>(out[k]) + off * tsz : p.hbuf[s][4 + k];
-      cudaError_t e = cudaMemcpyAsync(dst, dout[k], bytes, cudaMemcpyDeviceToHost, st);
-      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: D2H");
+    for (int o = 0; o < nops; o++) {
+      const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
+      for (int k = 0; k < 4; k++)
+        if (idx[4 * o + k] >= 0) din[k] = p.dbuf[s][idx[4 * o + k]];
+      void* dout[2] = {p.dbuf[s][U + 2 * o], p.dbuf[s][U + 2 * o + 1]};
+      if ((rc = ew_launch(ops[o], dtype, m, din, dout, st))) return rc;
+    }
+    for (int o = 0; o < 2 * nops; o++) {
+      void* dst = pin_out[o] ? static_cast<char*>(out[o]) + off * tsz : p.hbuf[s][U + o];
+      cudaError_t e = cudaMemcpyAsync(dst, p.dbuf[s][U + o], bytes, cudaMemcpyDeviceToHost, st);
+      if (e != cudaSuccess) return cuda_status(e, who);
     }
     cudaError_t e = cudaEventRecord(p.done[s], st);
-    if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: event");
+    if (e != cudaSuccess) return cuda_status(e, who);
     slot_off[s] = off;
   }
   // drain in chunk order
   for (int64_t c = nchunks; c < nchunks + S; c++)
     if ((rc = finish((int)(c % S)))) return rc;
   return TF_OK;
+}
+
+}  // namespace tf
+
+using namespace tf;
+
+extern "C" int tf_elementwise_host(int op, int dtype, int64_t n, const void* const* in,
+                                   void* const* out, int device) {
+  const int nin = ew_num_inputs(op);
+  if (nin < 0) return fail(TF_EINVAL, "tf_elementwise_host: unknown op id");
+  if (!in || !out) return fail(TF_EINVAL, "tf_elementwise_host: null plane");
+  const void* in4[4] = {nullptr, nullptr, nullptr, nullptr};
+  for (int k = 0; k < nin; k++) in4[k] = in[k];
+  return host_batch(1, &op, dtype, n, in4, out, device, "tf_elementwise_host");
+}
+
+extern "C" int tf_elementwise_host_batch(int nops, const int* ops, int dtype, int64_t n,
+                                         const void* const* in, void* const* out, int device) {
+  if (!ops) return fail(TF_EINVAL, "tf_elementwise_host_batch: null op list");
+  return host_batch(nops, ops, dtype, n, in, out, device, "tf_elementwise_host_batch");
 }

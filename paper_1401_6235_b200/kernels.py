@@ -302,3 +302,57 @@ def empty_twofold(n, dtype=np.float64, kind=TwofoldArray, device="cuda", pin_mem
 
 __all__ = ["TwofoldArray", "CoupledArray", "KernelSpec", "KERNELS",
            "empty_twofold"] + [row[0] for row in _TABLE]
+
+
+def host_batch(calls, device=None):
+    """Run several kernels on host (numpy) planes in ONE pipelined pass.
+
+    ``calls`` is a list of ``(name, *args, out)`` tuples with each kernel's own
+    signature, e.g. ``[("vtadd2", x, y, o1), ("vtsqrt1", x, o2)]``.  All planes
+    share one length and dtype.  Each distinct input plane crosses the host link
+    once per chunk however many calls read it; outputs come back in call order,
+    so the results equal running the calls one by one.  No output may overlap
+    any input of the batch (an intra-batch dependency), checked before any copy.
+    """
+    import ctypes
+
+    if not calls:
+        return
+    ops, ins, outs, first = [], [], [], None
+    for call in calls:
+        name, args = call[0], call[1:]
+        spec = KERNELS[name]
+        if spec.arity in ("22",):
+            (x0, x1), (y0, y1), (r0, r1) = args
+            planes = (x0, x1, y0, y1)
+        elif spec.arity == "21":
+            (x0, x1), y, (r0, r1) = args
+            planes = (x0, x1, y)
+        elif spec.arity == "11":
+            x, y, (r0, r1) = args
+            planes = (x, y)
+        elif spec.arity == "u2":
+            (x0, x1), (r0, r1) = args
+            planes = (x0, x1)
+        else:
+            x, (r0, r1) = args
+            planes = (x,)
+        desc = _check(name, planes, (r0, r1))
+        if any(d.kind != "host" for d in desc):
+            raise ValueError("%s: host_batch takes numpy (host) planes" % name)
+        if first is None:
+            first = desc[0]
+        elif desc[0].dtype != first.dtype or desc[0].n != first.n:
+            raise ValueError("%s: batch planes mix dtypes or lengths" % name)
+        ops.append(spec.core)
+        ins.extend([d.ptr for d in desc[:len(planes)]] + [None] * (4 - len(planes)))
+        outs.extend([d.ptr for d in desc[len(planes):]])
+    # cross-call aliasing (an output of one call over an input of another) is
+    # rejected by the library before any copy (TF_EINVAL -> ValueError)
+    L = _lib.lib()
+    dev = device if device is not None else (torch.cuda.current_device() if torch is not None else 0)
+    _lib.ensure_device(dev)
+    arr_ops = (ctypes.c_int * len(ops))(*ops)
+    rc = L.tf_elementwise_host_batch(len(ops), arr_ops, _dtype_id(first.dtype), first.n,
+                                     _lib.ptr_array(ins), _lib.ptr_array(outs), dev)
+    _lib.check(rc, "host_batch")

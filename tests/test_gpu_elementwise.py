@@ -311,3 +311,28 @@ def test_selftest_and_dotted_baselines():
         assert _lib.lib().tf_dotted(base, 1, n, x.data_ptr(), y.data_ptr(), r.data_ptr(), s) == 0
         torch.cuda.synchronize()
         assert torch.equal(r, ref), base
+
+
+def test_host_batch_matches_oracle_and_rejects_chains(oracle):
+    # several ops on host planes in one pipelined pass: shared inputs cross the
+    # link once, every op's outputs come back, results equal one-by-one calls
+    from paper_1401_6235_b200 import kernels as K
+
+    n = 3 * (1 << 21) + 11
+    a = _config2_inputs("vtadd2", n, 71)
+    d = _config2_inputs("vtdiv2", n, 72)
+    q = _config2_inputs("vtsqrt1", n, 73)
+    X, Y = K.TwofoldArray(a[0], a[1]), K.TwofoldArray(a[2], a[3])
+    outs = [K.empty_twofold(n, np.float64, device="cpu") for _ in range(4)]
+    pinned = K.empty_twofold(n, np.float64, device="cpu", pin_memory=True)
+    K.host_batch([("vtadd2", X, Y, outs[0]), ("vtmul2", X, Y, outs[1]),
+                  ("vtdiv2", X, K.TwofoldArray(d[2], d[3]), outs[2]),
+                  ("vtsqrt1", K.TwofoldArray(q[0], q[1]), outs[3]),
+                  ("vtsub2", X, Y, pinned)])
+    for o, (name, ins) in zip(outs + [pinned], [("vtadd2", a), ("vtmul2", a),
+                                                ("vtdiv2", (a[0], a[1], d[2], d[3])),
+                                                ("vtsqrt1", q), ("vtsub2", a)]):
+        w0, w1 = oracle.elementwise(name, *ins)
+        assert bits_equal(o.value, w0) and bits_equal(o.error, w1), name
+    with pytest.raises(ValueError, match="alias"):
+        K.host_batch([("vtadd2", X, Y, outs[0]), ("vtmul2", outs[0], Y, outs[1])])
