@@ -406,7 +406,7 @@ def run_elementwise(args, rank, world, local):
     import torch
 
     from paper_1401_6235_b200 import _lib
-    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import kernels as KM
 
     wl = WL[args.workload]
     n = args.n or wl["n"]
@@ -522,11 +522,11 @@ def run_elementwise(args, rank, world, local):
         # the same step as ONE host_batch call: each distinct host plane crosses
         # the link once per chunk (x, y shared by add/sub/mul/div)
         batch = [(op.name,) + op.host_args for op in ops]
-        K.host_batch(batch)
+        KM.host_batch(batch)
         barrier(world)
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            K.host_batch(batch)
+            KM.host_batch(batch)
         dtb = max_over_ranks(time.perf_counter() - t0, world)
         link = link_probe()
         hb = sum(op.h2d for op in ops) * args.e2e_steps
