@@ -62,8 +62,9 @@ def parse():
                     help="replay each step as a CUDA graph (auto: n <= 2^22, launch-bound)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 25,
-                    help="elements per op in the CPU baseline sample")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 26,
+                    help="elements per op in the CPU baseline sample (the reference arm "
+                         "generates min(this, 2^25) with numpy)")
     return ap.parse_args()
 
 
@@ -283,8 +284,10 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3):
-    """Oracle port (plain C, OpenMP, all host threads) on a bounded sample."""
+def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3, planes_of=None):
+    """Oracle port (plain C, OpenMP, all host threads) on a bounded sample.
+    planes_of(name) returns the op's host input planes (the first n_sample
+    elements of the bench's own device planes); else dists_host generates them."""
     from oracle import oracle as o
 
     rng = np.random.default_rng(99)
@@ -294,7 +297,7 @@ def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3):
     nt = os.cpu_count() or 1
     out = (np.zeros(n_sample, dtype), np.zeros(n_sample, dtype))
     for name in ops_names:
-        ins = dists_host(name, rng, n_sample)
+        ins = planes_of(name) if planes_of else dists_host(name, rng, n_sample)
         o.elementwise(name, *ins, nthreads=nt, out=out)  # warm-up (thread pool)
         best = None
         for _ in range(reps):
@@ -361,7 +364,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return 0
     wl = WL.get(args.workload, WL["config2"])
-    n_sample = min(args.n or wl["n"], args.cpu_sample)
+    n_sample = min(args.n or wl["n"], args.cpu_sample, 1 << 25)
     from oracle import oracle as o
 
     gen = host_dists(args.workload if args.workload in WL else "config2")
@@ -555,11 +558,16 @@ def run_elementwise(args, rank, world, local):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         log("cpu baseline")
         gen = host_dists(args.workload)
-        v, nt, per = cpu_baseline_elementwise(wl["names"], gen, dtype,
-                                              min(n, args.cpu_sample))
+        ns = min(n, args.cpu_sample)
+
+        def planes_of(name, ns=ns):  # the same inputs the GPU ran, first ns elements
+            return [p[:ns].cpu().numpy() for p in ps.planes(name)]
+
+        v, nt, per = cpu_baseline_elementwise(wl["names"], gen, dtype, ns, planes_of=planes_of)
         cpu = {"value": v, "unit": "elem-ops/s", "cores": nt, "kind": "port",
-               "sample": "%d elements per op over %s (best of 3 per op), oracle/twofold_oracle.c "
-                         "OpenMP on %d threads" % (min(n, args.cpu_sample), "/".join(wl["names"]), nt)}
+               "sample": "first %d elements of the bench's own input planes per op over %s "
+                         "(best of 3 per op), oracle/twofold_oracle.c OpenMP on %d threads"
+                         % (ns, "/".join(wl["names"]), nt)}
 
     log("done")
     if rank == 0:
