@@ -319,3 +319,149 @@ extern "C" int tf_elementwise_host_batch(int nops, const int* ops, int dtype, in
   if (!ops) return fail(TF_EINVAL, "tf_elementwise_host_batch: null op list");
   return host_batch(nops, ops, dtype, n, in, out, device, "tf_elementwise_host_batch");
 }
+
+// ---- reductions over host planes --------------------------------------------------
+namespace tf {
+size_t reduce_ws_bytes(int dtype, int64_t n);
+int reduce_geometry(int dtype, int* V, int* W, int* K);
+int reduce_launch(int rop, int dtype, int64_t n, const void* a, const void* b, void* out,
+                  void* ws, size_t ws_bytes, cudaStream_t s);
+int combine_launch(int dtype, int g, const void* partials, const int64_t* counts, void* out,
+                   cudaStream_t s);
+
+struct RedStage {
+  int64_t plane_bytes = 0;
+  void* d[HostPipe::MAX_SLOTS][2] = {};
+  void* h[HostPipe::MAX_SLOTS][2] = {};
+  void* ws[HostPipe::MAX_SLOTS] = {};
+  size_t ws_bytes = 0;
+};
+static RedStage g_red[64];
+}  // namespace tf
+
+// Reduce n elements of HOST planes (numpy) in the canonical order: chunks of C
+// tiles (C a power of two, so each chunk is a complete subtree of the tile tree)
+// stream through the slots; each chunk's subtree value lands in a device array
+// and the combine kernel folds them with the same adjacent-pair tree — the
+// result is bit-identical to tf_reduce on device planes.  Synchronous; writes
+// out[0..1] (host, dtype).
+extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, const void* b,
+                              void* out, int device) {
+  const char* who = "tf_reduce_host";
+  if (rop < 0 || rop >= TF_NUM_ROPS) return fail(TF_EINVAL, "tf_reduce_host: unknown reduction id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, "tf_reduce_host: planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, "tf_reduce_host: negative length");
+  if (!out) return fail(TF_EINVAL, "tf_reduce_host: null output");
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  if (n == 0) {
+    std::memset(out, 0, 2 * tsz);
+    return TF_OK;
+  }
+  if (!a || (rop != TF_RSUM && !b)) return fail(TF_EINVAL, "tf_reduce_host: null plane");
+  const int npl = rop == TF_RSUM ? 1 : 2;
+  const void* src[2] = {a, rop == TF_RSUM ? a : b};
+  DeviceGuard g(device);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(TF_EINVAL, "tf_reduce_host: device ordinal");
+  HostPipe& p = g_pipe[dev];
+  RedStage& R = g_red[dev];
+  std::lock_guard<std::mutex> lock(p.mu);
+  int rc = pipe_init(p);
+  if (rc) return rc;
+
+  int V = 0, W = 0, K = 0;
+  reduce_geometry(dtype, &V, &W, &K);
+  const int64_t L = (int64_t)V * W * K;
+  const int64_t T = (n + L - 1) / L;
+  int64_t C = 1;  // tiles per chunk: a power of two near the staging chunk size
+  while (C * L * (int64_t)tsz < p.chunk_bytes) C <<= 1;
+  while ((T + C - 1) / C > 1024) C <<= 1;  // the combine folds <= 1024 partials
+  const int64_t chunk = C * L;
+  const int64_t nchunks = (n + chunk - 1) / chunk;
+  const int64_t pbytes = chunk * (int64_t)tsz;
+
+  bool pin[2] = {is_pinned(src[0]), is_pinned(src[1])};
+  const bool pageable = !pin[0] || (npl == 2 && !pin[1]);
+  if (R.plane_bytes < pbytes || !R.ws[0]) {
+    for (int s = 0; s < HostPipe::MAX_SLOTS; s++) {
+      for (int k = 0; k < 2; k++) {
+        if (R.d[s][k]) cudaFree(R.d[s][k]);
+        if (R.h[s][k]) cudaFreeHost(R.h[s][k]);
+        R.d[s][k] = R.h[s][k] = nullptr;
+      }
+      if (R.ws[s]) cudaFree(R.ws[s]);
+      R.ws[s] = nullptr;
+    }
+    R.plane_bytes = pbytes;
+    R.ws_bytes = reduce_ws_bytes(dtype, chunk);
+    for (int s = 0; s < p.slots; s++) {
+      for (int k = 0; k < 2; k++) {
+        cudaError_t e = cudaMalloc(&R.d[s][k], pbytes);
+        if (e != cudaSuccess) return cuda_status(e, who);
+      }
+      cudaError_t e = cudaMalloc(&R.ws[s], R.ws_bytes);
+      if (e == cudaSuccess) e = cudaMemset(R.ws[s], 0, R.ws_bytes);
+      if (e != cudaSuccess) return cuda_status(e, who);
+    }
+  }
+  if (pageable) {
+    for (int s = 0; s < p.slots; s++)
+      for (int k = 0; k < 2; k++)
+        if (!R.h[s][k]) {
+          cudaError_t e = cudaHostAlloc(&R.h[s][k], pbytes, cudaHostAllocPortable);
+          if (e != cudaSuccess) return cuda_status(e, who);
+        }
+    if ((rc = ensure_planes(p, 0, true))) return rc;  // the copy pool
+  }
+  void* parts = nullptr;  // nchunks x 2 of dtype, then the result pair
+  cudaError_t e = cudaMalloc(&parts, (size_t)(nchunks + 1) * 2 * tsz);
+  if (e != cudaSuccess) return cuda_status(e, who);
+  std::vector<int64_t> counts(nchunks);
+  const int S = p.slots;
+  std::vector<char> busy(S, 0);
+  for (int64_t c = 0; c < nchunks; c++) {
+    const int s = (int)(c % S);
+    if (busy[s]) {  // the slot's previous chunk must be done before its buffers are reused
+      e = cudaEventSynchronize(p.done[s]);
+      if (e != cudaSuccess) { cudaFree(parts); return cuda_status(e, who); }
+    }
+    const int64_t off = c * chunk;
+    const int64_t m = (n - off) < chunk ? (n - off) : chunk;
+    counts[c] = m;
+    const size_t bytes = (size_t)m * tsz;
+    cudaStream_t st = p.st[s];
+    const void* din[2] = {nullptr, nullptr};
+    for (int k = 0; k < npl; k++) {
+      const void* from = static_cast<const char*>(src[k]) + off * tsz;
+      if (!pin[k]) {
+        par_memcpy(*p.pool, R.h[s][k], from, bytes);
+        from = R.h[s][k];
+      }
+      e = cudaMemcpyAsync(R.d[s][k], from, bytes, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) { cudaFree(parts); return cuda_status(e, who); }
+      din[k] = R.d[s][k];
+    }
+    rc = reduce_launch(rop, dtype, m, din[0], npl == 2 ? din[1] : nullptr,
+                       static_cast<char*>(parts) + (size_t)c * 2 * tsz, R.ws[s], R.ws_bytes, st);
+    if (rc) { cudaFree(parts); return rc; }
+    e = cudaEventRecord(p.done[s], st);
+    if (e != cudaSuccess) { cudaFree(parts); return cuda_status(e, who); }
+    busy[s] = 1;
+  }
+  for (int s = 0; s < S; s++)
+    if (busy[s] && (e = cudaEventSynchronize(p.done[s])) != cudaSuccess) {
+      cudaFree(parts);
+      return cuda_status(e, who);
+    }
+  void* res = static_cast<char*>(parts) + (size_t)nchunks * 2 * tsz;
+  rc = combine_launch(dtype, (int)nchunks, parts, counts.data(), res, p.st[0]);
+  if (!rc) {
+    e = cudaMemcpyAsync(out, res, 2 * tsz, cudaMemcpyDeviceToHost, p.st[0]);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p.st[0]);
+    if (e != cudaSuccess) rc = cuda_status(e, who);
+  }
+  cudaFree(parts);
+  return rc;
+}

@@ -69,8 +69,21 @@ def _reduce(name, rop, ins, out=None):
             raise ValueError("%s: planes mix %s and %s" % (name, first.dtype, p.dtype))
         if p.n != first.n:
             raise ValueError("%s: plane lengths differ (%d vs %d)" % (name, first.n, p.n))
+    if all(p.kind == "host" for p in planes):
+        # numpy planes: pipelined through the device by tf_reduce_host, same bits
+        if out is not None:
+            raise ValueError("%s: out= is for CUDA planes" % name)
+        dev = torch.cuda.current_device() if torch is not None else 0
+        _lib.ensure_device(dev)
+        dt = _dtype_id(first.dtype)
+        res = np.zeros(2, first.dtype)
+        rc = _lib.lib().tf_reduce_host(_lib.ROP_IDS[rop], dt, first.n, planes[0].ptr,
+                                       planes[1].ptr if len(planes) > 1 else None,
+                                       res.ctypes.data, dev)
+        _lib.check(rc, name)
+        return Twofold(float(res[0]), float(res[1]))
     if any(p.kind != "cuda" for p in planes):
-        raise ValueError("%s: reductions take CUDA tensors" % name)
+        raise ValueError("%s: planes mix host arrays and CUDA tensors" % name)
     if len({p.device for p in planes}) != 1:
         raise ValueError("%s: planes live on different devices" % name)
     dev = first.device
