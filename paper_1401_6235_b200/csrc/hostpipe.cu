@@ -183,6 +183,18 @@ static bool is_pinned(const void* ptr) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// On an error return, wait for everything already queued on the slot streams:
+// copies into the caller's host planes must not land after we have returned.
+struct DrainOnError {
+  HostPipe& p;
+  bool ok = false;
+  ~DrainOnError() {
+    if (ok) return;
+    for (int s = 0; s < p.slots; s++)
+      if (p.st[s]) cudaStreamSynchronize(p.st[s]);
+  }
+};
+
 // Run `nops` ops over the same n elements of host planes in one pipelined pass.
 // Distinct input planes (by address) cross the host link once per chunk however
 // many ops read them; every op's two outputs come back, in op order.
@@ -234,6 +246,7 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
   std::lock_guard<std::mutex> lock(p.mu);
   int rc = pipe_init(p);
   if (rc) return rc;
+  DrainOnError guard{p};
 
   const int U = (int)uniq.size();
   const int NP = U + 2 * nops;  // staging planes per slot: inputs, then outputs
@@ -297,6 +310,7 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
   // drain in chunk order
   for (int64_t c = nchunks; c < nchunks + S; c++)
     if ((rc = finish((int)(c % S)))) return rc;
+  guard.ok = true;
   return TF_OK;
 }
 
@@ -370,6 +384,7 @@ extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, cons
   std::lock_guard<std::mutex> lock(p.mu);
   int rc = pipe_init(p);
   if (rc) return rc;
+  DrainOnError guard{p};
 
   int V = 0, W = 0, K = 0;
   reduce_geometry(dtype, &V, &W, &K);
@@ -462,6 +477,9 @@ extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, cons
     if (e == cudaSuccess) e = cudaStreamSynchronize(p.st[0]);
     if (e != cudaSuccess) rc = cuda_status(e, who);
   }
+  if (!rc) guard.ok = true;
+  else
+    for (int s = 0; s < p.slots; s++) cudaStreamSynchronize(p.st[s]);
   cudaFree(parts);
   return rc;
 }

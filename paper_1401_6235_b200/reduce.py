@@ -34,7 +34,10 @@ except Exception:  # pragma: no cover
 
 Twofold = namedtuple("Twofold", ("value", "error"))
 
-_WS = {}  # (device, dtype) -> workspace tensor (zeroed once; the kernel leaves it zeroed)
+# (device, dtype, stream) -> workspace tensor, zeroed once (the kernel leaves it
+# zeroed).  Keyed by stream: reductions on different streams may run concurrently
+# and must not share the tile-partial array or the ticket counter.
+_WS = {}
 
 
 def geometry(dtype=np.float64):
@@ -51,12 +54,14 @@ def tile_elems(dtype=np.float64) -> int:
     return V * W * K
 
 
-def workspace(device: int, dtype_id: int, n: int):
+def workspace(device: int, dtype_id: int, n: int, stream=None):
     need = _lib.lib().tf_reduce_workspace_bytes(0, dtype_id, n)
-    key = (device, dtype_id)
+    stream = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (device, dtype_id, stream.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
-        ws = torch.zeros(max(need, 4096), dtype=torch.uint8, device="cuda:%d" % device)
+        with torch.cuda.stream(stream):  # allocated, zeroed and used on one stream
+            ws = torch.zeros(max(need, 4096), dtype=torch.uint8, device="cuda:%d" % device)
         _WS[key] = ws
     return ws
 
