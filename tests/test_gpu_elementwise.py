@@ -336,3 +336,27 @@ def test_host_batch_matches_oracle_and_rejects_chains(oracle):
         assert bits_equal(o.value, w0) and bits_equal(o.error, w1), name
     with pytest.raises(ValueError, match="alias"):
         K.host_batch([("vtadd2", X, Y, outs[0]), ("vtmul2", outs[0], Y, outs[1])])
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+def test_all_ops_on_random_bit_patterns(oracle, fmt):
+    # every IEEE class (subnormals, infinities, NaNs, signed zeros, huge/tiny
+    # magnitudes) drawn from raw bit patterns: device == oracle, NaN by position
+    from paper_1401_6235_b200 import kernels as K
+
+    dtype = np.float64 if fmt == "f64" else np.float32
+    u = np.uint64 if fmt == "f64" else np.uint32
+    rng = np.random.default_rng(31337)
+    n = 200_003
+    for name in list(K.KERNELS) + ["div_rem", "sqrt_resid"]:
+        nin = oracle.NUM_INPUTS[name]
+        ins = []
+        for _ in range(nin):
+            raw = rng.integers(0, np.iinfo(u).max, n, dtype=u, endpoint=True).view(dtype)
+            ordinary = (rng.uniform(-4, 4, n) * np.exp2(rng.integers(-40, 40, n))).astype(dtype)
+            ins.append(np.where(rng.random(n) < 0.5, raw, ordinary).astype(dtype))
+        with np.errstate(all="ignore"):
+            w0, w1 = oracle.elementwise(name, *ins)
+        r0, r1 = run_device(name, ins)
+        assert bits_equal(r0, w0), (name, first_mismatch(r0, w0))
+        assert bits_equal(r1, w1), (name, first_mismatch(r1, w1))
