@@ -119,7 +119,7 @@ static void par_memcpy(CopyPool& pool, void* dst, const void* src, size_t bytes)
 struct HostPipe {
   static constexpr int MAX_SLOTS = 8;
   int slots = 3;
-  int64_t chunk_bytes = 16ll << 20;  // per plane per slot
+  int64_t chunk_bytes = 32ll << 20;  // per plane per slot (sweep: 32 MB best, r1 profiles)
   std::mutex mu;
   bool ready = false;
   cudaStream_t st[MAX_SLOTS] = {};
