@@ -17,7 +17,10 @@ Keys beyond the base contract:
   cpu_baseline  the CPU oracle port (oracle/, all host threads) on a bounded
                 sample of the same workload, rank 0 at N=1 only
   e2e           the same metric through the public API with pinned HOST planes
-                (kernels.vtadd2(numpy...) -> tf_elementwise_host), H2D and D2H inside
+                (kernels.vtadd2(numpy...) -> tf_elementwise_host), H2D and D2H inside,
+                on the first 2^27 elements of each plane (PCIe-bound rate); its
+                roofline is the live-measured host link for the step's traffic mix;
+                e2e.batched = the same step as one kernels.host_batch call
   per_op        per-kernel CUDA-event times and GB/s
   clocks        NVML SM clock + event reasons sampled during the timed region
 
@@ -42,10 +45,6 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "twofold elem-ops/s & achieved HBM GB/s (fp64) at 1/2/4/8 B200 vs CPU oracle"
-
-# op -> (inputs, bytes/elem f64)
-NIN = {"vtadd2": 4, "vtsub2": 4, "vtmul2": 4, "vtdiv2": 4, "vtsqrt1": 2}
-
 
 def parse():
     ap = argparse.ArgumentParser()

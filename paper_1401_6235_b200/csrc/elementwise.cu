@@ -7,13 +7,15 @@
 // (NIN + 2) * sizeof(T) bytes and nothing else.
 //
 // Layout in HBM: each plane is one contiguous 1-D array (SoA, kernels.py:3-5).
-// Design: a persistent grid (resident CTAs only, sized by the occupancy
-// calculator for 148 SMs) grid-strides over 16-byte vectors; each thread
-// issues UNROLL x NIN independent 128-bit streaming loads before any math, so
-// every SM keeps >= 64 KB of reads in flight.  Planes that share a common
-// misalignment get a scalar head; the n % (16/sizeof(T)) tail is scalar too —
-// both handled by the same launch.  Planes with different misalignments run
-// the scalar grid-stride path (still one launch).
+// Design: one CTA per chunk of 256*U*4 vectors, so the hardware block scheduler
+// balances the 148 SMs (a persistent grid left a tail of idle SMs: -6..7 points
+// of bandwidth, profiles/README.md).  Vectors are 32 bytes — sm_100's 256-bit
+// LDG/STG (LDG.E.NA.EFL2.256 / STG.E.EF.ENL2.256) — and each thread issues
+// U x NIN independent streaming loads before any math.  Planes that share a
+// common misalignment get a scalar head; the n % (32/sizeof(T)) tail is scalar
+// too — both in the same launch.  Planes with different misalignments run the
+// scalar grid-stride path (still one launch).  TF_VEC_BYTES=16 and
+// TF_EW_SCHED=persistent select the earlier variants for A/B measurements.
 #include <cuda_runtime.h>
 
 #include <cstdlib>
