@@ -5,6 +5,7 @@ marks in scope:
   crit 4  exact transforms are error-free (test_acceptance.py:190-245)
   crit 5  the value plane bitwise shadows plain arithmetic (:252-322)
   crit 7  coupling invariants |e| <= ulp(v)/2 and exact renormalization (:359-381)
+  crit 9  twofold/dotted throughput ratios on the GPU harness (:424-441)
   crit 10 batch kernels equal the scalar cores at n in {100, 1e4, 1e6} (:448-484)
 The gmpy2 rationals of the reference's oracle.py become fractions.Fraction here
 (gmpy2 is absent from this image); "scalar cores" become the pinned oracle.
