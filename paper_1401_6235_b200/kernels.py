@@ -180,9 +180,17 @@ def _dtype_id(dt) -> int:
     return _lib.TF_F64 if dt == np.dtype(np.float64) else _lib.TF_F32
 
 
+def _raw_stream(dev):
+    """cudaStream_t of torch's current stream on `dev` (no Stream object)."""
+    try:
+        return torch._C._cuda_getCurrentRawStream(dev)
+    except AttributeError:  # pragma: no cover - older torch
+        return torch.cuda.current_stream(dev).cuda_stream
+
+
 def _launch(name, op, planes, nin):
     """Raw launch over described planes (device: async; host: synchronous)."""
-    L = _lib.lib()
+    L = _lib._lib or _lib.lib()
     first = planes[0]
     n = first.n
     if n == 0:
@@ -191,11 +199,16 @@ def _launch(name, op, planes, nin):
     outs = _lib.ptr_array([p.ptr for p in planes[nin:]])
     if first.kind == "cuda":
         dev = first.device
-        _lib.ensure_device(dev)
-        stream = torch.cuda.current_stream(dev).cuda_stream
-        with torch.cuda.device(dev):
+        if dev not in _lib._selftested:
+            _lib.ensure_device(dev)
+        stream = _raw_stream(dev)
+        if torch.cuda.current_device() == dev:
             rc = L.tf_elementwise(op, _dtype_id(first.dtype), n, ins, outs, stream)
-        _lib.check(rc, name)
+        else:
+            with torch.cuda.device(dev):
+                rc = L.tf_elementwise(op, _dtype_id(first.dtype), n, ins, outs, stream)
+        if rc:
+            _lib.check(rc, name)
     else:
         dev = torch.cuda.current_device() if torch is not None else 0
         _lib.ensure_device(dev)
