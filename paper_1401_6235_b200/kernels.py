@@ -120,22 +120,32 @@ def _is_tensor(a) -> bool:
     return torch is not None and isinstance(a, torch.Tensor)
 
 
+_F64, _F32 = np.dtype(np.float64), np.dtype(np.float32)
+_TORCH_DT = {}
+if torch is not None:
+    _TORCH_DT = {torch.float64: _F64, torch.float32: _F32}
+    _Tensor = torch.Tensor
+else:  # pragma: no cover
+    _Tensor = ()
+
+
 def _describe(name, a) -> _Plane:
+    if isinstance(a, _Tensor):  # the hot path: one call per plane per launch
+        dt = _TORCH_DT.get(a.dtype)
+        if a.dim() != 1 or not a.is_contiguous():
+            raise ValueError("%s: planes must be 1-D and contiguous" % name)
+        if dt is None:
+            raise ValueError("%s: planes must be float32 or float64, got %s" % (name, a.dtype))
+        dev = a.get_device()
+        if dev >= 0:
+            return _Plane(a, "cuda", dt, a.shape[0], a.data_ptr(), a.nbytes, dev)
+        return _Plane(a, "host", dt, a.shape[0], a.data_ptr(), a.nbytes, None)
     if isinstance(a, np.ndarray):
         if a.ndim != 1 or not a.flags.c_contiguous:
             raise ValueError("%s: planes must be 1-D and contiguous" % name)
         if a.dtype not in _NP_DTYPES:
             raise ValueError("%s: planes must be float32 or float64, got %s" % (name, a.dtype))
         return _Plane(a, "host", a.dtype, a.shape[0], a.ctypes.data, a.nbytes, None)
-    if _is_tensor(a):
-        if a.dim() != 1 or not a.is_contiguous():
-            raise ValueError("%s: planes must be 1-D and contiguous" % name)
-        if a.dtype not in (torch.float32, torch.float64):
-            raise ValueError("%s: planes must be float32 or float64, got %s" % (name, a.dtype))
-        dt = np.dtype(np.float64) if a.dtype == torch.float64 else np.dtype(np.float32)
-        kind = "cuda" if a.is_cuda else "host"
-        dev = a.device.index if a.is_cuda else None
-        return _Plane(a, kind, dt, a.shape[0], a.data_ptr(), a.numel() * a.element_size(), dev)
     raise ValueError("%s: planes must be numpy arrays or CUDA tensors, got %r"
                      % (name, type(a).__name__))
 
