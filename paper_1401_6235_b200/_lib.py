@@ -9,10 +9,12 @@ every entry point raises.  ctypes releases the GIL for the duration of each call
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libtwofold_b200.so"
+LIB_PATH = Path(os.environ.get("TF_LIB_PATH") or
+                (Path(__file__).resolve().parent / "_lib" / "libtwofold_b200.so"))
 
 TF_OK, TF_EINVAL, TF_ECUDA, TF_ENOMEM, TF_ESELFTEST = 0, -1, -2, -3, -4
 TF_F32, TF_F64 = 0, 1

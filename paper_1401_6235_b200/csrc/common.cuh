@@ -9,6 +9,11 @@
 
 #include "../../include/twofold_b200.h"
 
+// store cache hint (".cs" streaming by default; A/B builds may override)
+#ifndef TF_ST_HINT
+#define TF_ST_HINT ".cs"
+#endif
+
 namespace tf {
 
 // thread-local last error, surfaced through tf_last_error()
@@ -62,18 +67,18 @@ __device__ __forceinline__ float ld_stream(const float* p) {
   return v;
 }
 __device__ __forceinline__ void st_stream(double2* p, double2 v) {
-  asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+  asm volatile("st.global" TF_ST_HINT ".v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 __device__ __forceinline__ void st_stream(float4* p, float4 v) {
-  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+  asm volatile("st.global" TF_ST_HINT ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
                : "memory");
 }
 __device__ __forceinline__ void st_stream(double* p, double v) {
-  asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  asm volatile("st.global" TF_ST_HINT ".f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 __device__ __forceinline__ void st_stream(float* p, float v) {
-  asm volatile("st.global.cs.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+  asm volatile("st.global" TF_ST_HINT ".f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
 }
 
 // 16-byte vector of a plane type
@@ -133,12 +138,12 @@ __device__ __forceinline__ Vec32<float> ld_stream(const Vec32<float>* p) {
   return r;
 }
 __device__ __forceinline__ void st_stream(Vec32<double>* p, const Vec32<double>& r) {
-  asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]),
+  asm volatile("st.global" TF_ST_HINT ".v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]),
                "d"(r.v[2]), "d"(r.v[3])
                : "memory");
 }
 __device__ __forceinline__ void st_stream(Vec32<float>* p, const Vec32<float>& r) {
-  asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
+  asm volatile("st.global" TF_ST_HINT ".v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r.v[0]),
                "f"(r.v[1]), "f"(r.v[2]), "f"(r.v[3]), "f"(r.v[4]), "f"(r.v[5]), "f"(r.v[6]),
                "f"(r.v[7])
                : "memory");
@@ -162,10 +167,10 @@ __device__ __forceinline__ Vec16A<float> ld_stream(const Vec16A<float>* p) {
   return r;
 }
 __device__ __forceinline__ void st_stream(Vec16A<double>* p, const Vec16A<double>& r) {
-  asm volatile("st.global.cs.v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]) : "memory");
+  asm volatile("st.global" TF_ST_HINT ".v2.f64 [%0], {%1,%2};" ::"l"(p), "d"(r.v[0]), "d"(r.v[1]) : "memory");
 }
 __device__ __forceinline__ void st_stream(Vec16A<float>* p, const Vec16A<float>& r) {
-  asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]),
+  asm volatile("st.global" TF_ST_HINT ".v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r.v[0]), "f"(r.v[1]),
                "f"(r.v[2]), "f"(r.v[3])
                : "memory");
 }
