@@ -731,6 +731,18 @@ def run_config5(args, rank, world, local):
     instr = 220.0 * n
     achieved = instr / (per_ms * 1e-3)
     value = world * n * K / (elapsed_ms * 1e-3)
+    # e2e: the public API on pinned numpy planes (tf_horner_host pipeline)
+    ne = min(n, E2E_MAX)
+    xh = torch.empty(ne, dtype=torch.float64, pin_memory=True)
+    xh.copy_(x[:ne])
+    xh = xh.numpy()
+    oh = Kmod.empty_twofold(ne, np.float64, device="cpu", pin_memory=True)
+    R.vthorner(c, xh, oh)
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        R.vthorner(c, xh, oh)
+    dte = max_over_ranks(time.perf_counter() - t0, world)
     if rank == 0:
         line = {
             "metric": "twofold Horner points/s (fp64, (x-1)^20)", "value": value, "unit": "points/s",
@@ -744,6 +756,10 @@ def run_config5(args, rank, world, local):
                          "frac": achieved / fp64_peak, "traffic": ncu_traffic("vthorner"),
                          "algorithmic_instr": instr,
                          "peak_source": "measured live: tf_fp64_peak (independent DFMA chains)"},
+            "e2e": {"value": world * ne * args.e2e_steps / dte, "unit": "points/s",
+                    "h2d_bytes_per_step": 8 * ne, "d2h_bytes_per_step": 16 * ne,
+                    "elems_per_step": ne,
+                    "path": "reduce.vthorner on pinned numpy planes -> tf_horner_host"},
             "gpu_launches": world * K,
             "clocks": clk.summary(),
         }

@@ -198,8 +198,11 @@ struct DrainOnError {
 // Run `nops` ops over the same n elements of host planes in one pipelined pass.
 // Distinct input planes (by address) cross the host link once per chunk however
 // many ops read them; every op's two outputs come back, in op order.
+using HostLaunch = std::function<int(int, int64_t, const void* const*, void* const*, cudaStream_t)>;
+
 static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void* const* in,
-                      void* const* out, int device, const char* who) {
+                      void* const* out, int device, const char* who,
+                      const HostLaunch* launch = nullptr, int nin_all = -1) {
   if (nops < 1 || nops > 64) return fail(TF_EINVAL, std::string(who) + ": 1..64 ops per batch");
   if (dtype != TF_F32 && dtype != TF_F64)
     return fail(TF_EINVAL, std::string(who) + ": planes must be float32 or float64");
@@ -210,7 +213,7 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
   std::vector<const void*> uniq;
   std::vector<int> idx((size_t)nops * 4, -1);
   for (int o = 0; o < nops; o++) {
-    const int nin = ew_num_inputs(ops[o]);
+    const int nin = nin_all >= 0 ? nin_all : ew_num_inputs(ops[o]);
     if (nin < 0) return fail(TF_EINVAL, std::string(who) + ": unknown op id");
     if (!out[2 * o] || !out[2 * o + 1]) return fail(TF_EINVAL, std::string(who) + ": null plane");
     for (int k = 0; k < nin; k++) {
@@ -296,7 +299,8 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
       for (int k = 0; k < 4; k++)
         if (idx[4 * o + k] >= 0) din[k] = p.dbuf[s][idx[4 * o + k]];
       void* dout[2] = {p.dbuf[s][U + 2 * o], p.dbuf[s][U + 2 * o + 1]};
-      if ((rc = ew_launch(ops[o], dtype, m, din, dout, st))) return rc;
+      rc = launch ? (*launch)(o, m, din, dout, st) : ew_launch(ops[o], dtype, m, din, dout, st);
+      if (rc) return rc;
     }
     for (int o = 0; o < 2 * nops; o++) {
       void* dst = pin_out[o] ? static_cast<char*>(out[o]) + off * tsz : p.hbuf[s][U + o];
@@ -326,6 +330,27 @@ extern "C" int tf_elementwise_host(int op, int dtype, int64_t n, const void* con
   const void* in4[4] = {nullptr, nullptr, nullptr, nullptr};
   for (int k = 0; k < nin; k++) in4[k] = in[k];
   return host_batch(1, &op, dtype, n, in4, out, device, "tf_elementwise_host");
+}
+
+namespace tf {
+int horner_launch(int dtype, int64_t n, const void* x, const double* coeffs, int degree,
+                  void* o0, void* o1, cudaStream_t s);
+}
+
+// Twofold Horner over HOST planes through the same pipeline (x in, z0/z1 out).
+extern "C" int tf_horner_host(int dtype, int64_t n, const void* x, const double* coeffs,
+                              int degree, void* out0, void* out1, int device) {
+  if (!coeffs || degree < 0 || degree > TF_HORNER_MAX_DEGREE)
+    return fail(TF_EINVAL, "tf_horner_host: degree out of range or null coefficients");
+  std::vector<double> c(coeffs, coeffs + degree + 1);
+  HostLaunch fn = [&](int, int64_t m, const void* const* din, void* const* dout,
+                      cudaStream_t st) {
+    return horner_launch(dtype, m, din[0], c.data(), degree, dout[0], dout[1], st);
+  };
+  const void* in4[4] = {x, nullptr, nullptr, nullptr};
+  void* out2[2] = {out0, out1};
+  int op = 0;
+  return host_batch(1, &op, dtype, n, in4, out2, device, "tf_horner_host", &fn, 1);
 }
 
 extern "C" int tf_elementwise_host_batch(int nops, const int* ops, int dtype, int64_t n,

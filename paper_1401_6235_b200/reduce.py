@@ -152,13 +152,18 @@ def vthorner(coeffs, x, out):
     r0, r1 = out
     planes = _check("vthorner", (x,), (r0, r1))
     first = planes[0]
-    if first.kind != "cuda":
-        raise ValueError("vthorner: planes must be CUDA tensors")
     if first.n == 0:
+        return
+    carr = (ctypes.c_double * len(c))(*c)
+    if first.kind == "host":  # numpy planes: through the host pipeline (tf_horner_host)
+        dev = torch.cuda.current_device() if torch is not None else 0
+        _lib.ensure_device(dev)
+        rc = _lib.lib().tf_horner_host(_dtype_id(first.dtype), first.n, first.ptr, carr,
+                                       len(c) - 1, planes[1].ptr, planes[2].ptr, dev)
+        _lib.check(rc, "vthorner")
         return
     dev = first.device
     _lib.ensure_device(dev)
-    carr = (ctypes.c_double * len(c))(*c)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream
         rc = _lib.lib().tf_horner(_dtype_id(first.dtype), first.n, first.ptr, carr, len(c) - 1,

@@ -254,3 +254,17 @@ def test_host_plane_reductions_match_device(oracle, rop, pin):
     zd = fn(_t(x), _t(y))
     w = oracle.reduce(rop, x, None if rop == "sum" else y, geometry=_geom(np.float64))
     assert (zh.value, zh.error) == (zd.value, zd.error) == (float(w[0]), float(w[1]))
+
+
+def test_horner_host_planes_match_device(oracle):
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+
+    n = 3 * (1 << 22) + 5
+    x = np.random.default_rng(12).uniform(0.9, 1.1, n)
+    c = R.binomial_coeffs(20)
+    out = K.empty_twofold(n, np.float64, device="cpu")
+    R.vthorner(c, x, out)
+    w0, w1 = oracle.horner(c, x)
+    assert np.array_equal(out.value.view(np.uint64), w0.view(np.uint64))
+    assert np.array_equal(out.error.view(np.uint64), w1.view(np.uint64))
