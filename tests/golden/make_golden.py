@@ -392,7 +392,7 @@ def make_accumulate_kat():
     print("accumulate KAT:", kat)
 
 
-if __name__ == "__main__" and "fused" not in sys.argv:
+if __name__ == "__main__" and len(sys.argv) == 1:
     make_elementwise()
     make_reductions()
     make_horner()
@@ -528,5 +528,39 @@ def make_fused():
     print("fused fixtures written")
 
 
-if __name__ == "__main__" and "fused" in sys.argv:
+if __name__ == "__main__" and ("fused" in sys.argv or len(sys.argv) == 1):
     make_fused()
+
+
+# --------------------------------------------------------------------------
+# config-size hashes: the reference's own outputs on BASELINE-distributed inputs
+
+
+def _cfg_inputs(config, name, n, seed):
+    sys.path.insert(0, str(OUT))
+    from config_inputs import cfg_inputs
+
+    return cfg_inputs(config, name, n, seed)
+
+
+def make_config_hashes():
+    cases = []
+    plan = [("config1", ["vtadd2", "vtmul2"], 1 << 20),
+            ("config2", ["vtadd2", "vtsub2", "vtmul2", "vtdiv2", "vtsqrt1"], 1 << 22),
+            ("config3", ["vtadd2", "vtmul2", "vtdiv2"], 1 << 22)]
+    for config, names, n in plan:
+        for j, name in enumerate(names):
+            seed = 7000 + 10 * j + int(config[-1])
+            ins = _cfg_inputs(config, name, n, seed)
+            dtype = ins[0].dtype
+            r0, r1 = _run_reference(name, ins, dtype)
+            cases.append(dict(config=config, op=name, n=n, seed=seed, dtype=str(dtype),
+                              numpy=np.__version__, sha_in=_sha(*ins),
+                              sha_z0=hashlib.sha256(r0.tobytes()).hexdigest(),
+                              sha_z1=hashlib.sha256(r1.tobytes()).hexdigest()))
+    (OUT / "config_hashes.json").write_text(json.dumps(cases, indent=1))
+    print("config hashes:", len(cases))
+
+
+if __name__ == "__main__" and ("hashes" in sys.argv or len(sys.argv) == 1):
+    make_config_hashes()
