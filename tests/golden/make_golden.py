@@ -311,7 +311,7 @@ def make_reductions():
                 L = geom[0] * geom[1] * geom[2]
                 sizes = sorted({0, 1, 2, 3, L - 1, L, L + 1, 2 * L + 5, 7 * L + 3, 16 * L})
                 if geom == prod[fmt]:
-                    sizes = [0, 1, 5, 1000, L - 3, L, L + 1, 3 * L + 12345]
+                    sizes = [0, 1, 5, 1000, L - 3, L, L + 1, 3 * L + 12345, (1 << 24) + 17]
                 for n in sizes:
                     kind = "wide" if (idx % 2) else "uniform"
                     seed = 5000 + idx
