@@ -1,0 +1,42 @@
+"""Past 2^31 elements: 64-bit indexing in every kernel family (B200, ~70 GB HBM).
+
+Elementwise: vtadd (TwoSum) over 2^31+5 f32 elements checked on the device
+against TwoSum evaluated with plain torch ops (each an IEEE-RN kernel, no
+contraction), and the twofold sum of the same plane bit-exact against the oracle.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = [pytest.mark.gpu, pytest.mark.fullsize]
+
+N = (1 << 31) + 5
+
+
+def test_elementwise_and_reduction_past_2g_elements(oracle):
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+    from paper_1401_6235_b200 import workloads as W
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 80e9:
+        pytest.skip("needs ~80 GB of free HBM")
+    x = W.fill(torch.empty(N, dtype=torch.float32, device="cuda"), W.LOGU_SIGNED, 11, 0, -20.0, 20.0)
+    y = W.fill(torch.empty(N, dtype=torch.float32, device="cuda"), W.LOGU_SIGNED, 12, 0, -20.0, 20.0)
+    z = K.empty_twofold(N, torch.float32, K.CoupledArray)
+    K.vtadd(x, y, z)
+    s = x + y
+    assert torch.equal(z.value, s)
+    bv = s - x
+    av = s - bv
+    t = (x - av) + (y - bv)
+    del s, bv, av
+    assert torch.equal(z.error, t)
+    del t, z, y
+    torch.cuda.empty_cache()
+    zs = R.vtsum(x)
+    xh = x.cpu().numpy()
+    w = oracle.reduce("sum", xh, geometry=R.geometry(np.float32))
+    assert (zs.value, zs.error) == (float(w[0]), float(w[1]))
