@@ -31,7 +31,10 @@ namespace tf {
 
 constexpr int RW = 256;  // lanes per tile
 constexpr int RK = 128;  // vectors per lane
-constexpr int RKB = 8;   // vectors per load batch
+constexpr int RKB = 8;   // vectors per load batch (two planes)
+#ifndef TF_RKB_SUM
+#define TF_RKB_SUM 16        // one plane: twice the batch keeps the same bytes in flight
+#endif
 
 template <class T>
 struct Geo {
@@ -208,20 +211,22 @@ __global__ void __launch_bounds__(RW) reduce_kernel(const T* __restrict__ a,
     // full tile, 16-byte aligned planes
     const Vt* va = reinterpret_cast<const Vt*>(a + base) + w;
     const Vt* vb = reinterpret_cast<const Vt*>((ROP == TF_RSUM ? a : b) + base) + w;
+    constexpr int KB = ROP == TF_RSUM ? TF_RKB_SUM : RKB;
 #pragma unroll 1
-    for (int k0 = 0; k0 < RK; k0 += RKB) {
-      Vt ra[RKB], rb[RKB];
+    for (int k0 = 0; k0 < RK; k0 += KB) {
+      Vt ra[KB], rb[ROP == TF_RSUM ? 1 : KB];
 #pragma unroll
-      for (int kb = 0; kb < RKB; kb++) {
+      for (int kb = 0; kb < KB; kb++) {
         ra[kb] = ld_stream(va + (int64_t)RW * (k0 + kb));
         if constexpr (ROP != TF_RSUM) rb[kb] = ld_stream(vb + (int64_t)RW * (k0 + kb));
       }
 #pragma unroll
-      for (int kb = 0; kb < RKB; kb++) {
+      for (int kb = 0; kb < KB; kb++) {
 #pragma unroll
         for (int e = 0; e < V; e++) {
           T x = lane<T>(ra[kb], e);
-          T y = (ROP == TF_RSUM) ? x : lane<T>(rb[kb], e);
+          T y = x;
+          if constexpr (ROP != TF_RSUM) y = lane<T>(rb[kb], e);
           if (k0 == 0 && kb == 0 && e == 0) acc = first_term<T, ROP>(x, y);
           else acc = fold<T, ROP>(acc, x, y);
         }
