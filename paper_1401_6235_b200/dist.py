@@ -73,7 +73,8 @@ def gather_partials(partial, group=None):
 
 def sharded_reduce(rop: str, local: Sequence, n: int, group=None,
                    reduce_fn: Optional[Callable] = None,
-                   combine_fn: Optional[Callable] = None, tile: Optional[int] = None):
+                   combine_fn: Optional[Callable] = None, tile: Optional[int] = None,
+                   transport=None):
     """Reduce a globally sharded plane set; every rank returns the same Twofold.
 
     ``local`` holds this rank's planes (its shard_tiles slice).  reduce_fn /
@@ -102,6 +103,11 @@ def sharded_reduce(rop: str, local: Sequence, n: int, group=None,
             part.zero_()
     else:
         part = reduce_fn(rop, local)
+    if transport is not None:  # NVLink peer-memory combine (P2PTransport), no NCCL
+        counts = shard_counts(n, world, tile)
+        transport.combine(part, counts)
+        v = part.cpu().tolist()
+        return R.Twofold(v[0], v[1])
     allp = gather_partials(part, group)
     counts = shard_counts(n, world, tile)
     if combine_fn is None:
@@ -110,4 +116,52 @@ def sharded_reduce(rop: str, local: Sequence, n: int, group=None,
 
 
 __all__ = ["shard_elementwise", "shard_tiles", "shard_counts", "gather_partials",
-           "sharded_reduce"]
+           "sharded_reduce", "P2PTransport"]
+
+
+class P2PTransport:
+    """Cross-GPU combine over NVLink peer memory, without NCCL (opt-in).
+
+    Every rank maps every other rank's mailbox through CUDA IPC; after the
+    local reduction one device thread stores the 16-byte partial into all
+    peers' mailboxes, waits for all of theirs and folds them with the same
+    adjacent-pair tree as ``tf_combine`` (csrc/xgpu.cu), so results are
+    bit-identical to the NCCL path.  Collective: every rank constructs it and
+    calls ``combine`` the same number of times.  With no process group (or a
+    world of 1) it runs single-rank, which is how it is tested on one GPU.
+    """
+
+    def __init__(self, group=None, device=None):
+        import ctypes
+
+        from . import _lib
+
+        self._lib = _lib
+        self.dev = torch.cuda.current_device() if device is None else device
+        _lib.ensure_device(self.dev)
+        use_dist = dist is not None and dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if use_dist else 1
+        self.rank = dist.get_rank(group) if use_dist else 0
+        h = (ctypes.c_char * 64)()
+        _lib.check(_lib.lib().tf_xgpu_mailbox(self.dev, h), "P2PTransport")
+        handles = [bytes(h)]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, bytes(h), group=group)
+        blob = b"".join(handles)
+        _lib.check(_lib.lib().tf_xgpu_open(self.dev, self.world, self.rank, blob), "P2PTransport")
+
+    def combine(self, partial, counts):
+        """partial: this rank's 2-element CUDA tensor (overwritten with the result)."""
+        import ctypes
+
+        dt = self._lib.TF_F64 if partial.dtype == torch.float64 else self._lib.TF_F32
+        c = (ctypes.c_int64 * self.world)(*[int(v) for v in counts])
+        with torch.cuda.device(partial.device):
+            s = torch.cuda.current_stream(partial.device).cuda_stream
+            rc = self._lib.lib().tf_xgpu_combine(dt, partial.data_ptr(), c, s)
+        self._lib.check(rc, "P2PTransport.combine")
+        return partial
+
+    def status(self):
+        return self._lib.lib().tf_xgpu_status(self.dev)

@@ -268,3 +268,27 @@ def test_horner_host_planes_match_device(oracle):
     w0, w1 = oracle.horner(c, x)
     assert np.array_equal(out.value.view(np.uint64), w0.view(np.uint64))
     assert np.array_equal(out.error.view(np.uint64), w1.view(np.uint64))
+
+
+def test_p2p_transport_single_rank_matches_combine():
+    # the NVLink mailbox combine (csrc/xgpu.cu) at world 1: publish, wait, fold;
+    # repeated calls alternate the epoch-parity buffers
+    from paper_1401_6235_b200 import dist as D
+    from paper_1401_6235_b200 import reduce as R
+
+    tp = D.P2PTransport()
+    rng = np.random.default_rng(4)
+    for trial in range(5):
+        n = 3 * 65536 + 17 * trial
+        x = _t(rng.uniform(-1, 1, n) * np.exp2(rng.integers(-20, 21, n)))
+        want = R.vtsum(x)
+        part = torch.empty(2, dtype=torch.float64, device=DEV)
+        R.vtsum(x, out=part)
+        tp.combine(part, [n])
+        assert (part[0].item(), part[1].item()) == (want.value, want.error)
+        part32 = torch.empty(2, dtype=torch.float32, device=DEV)
+        R.vtsum(x.float(), out=part32)
+        w32 = R.vtsum(x.float())
+        tp.combine(part32, [n])
+        assert (part32[0].item(), part32[1].item()) == (w32.value, w32.error)
+    assert tp.status() == 0
