@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step as a CUDA graph (auto: n <= 2^22, launch-bound)")
+    ap.add_argument("--reduce-transport", choices=["nccl", "p2p"], default="nccl",
+                    help="config4 cross-GPU combine: NCCL all-gather + tf_combine, or the "
+                         "NVLink peer-memory mailboxes (csrc/xgpu.cu)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26,
@@ -626,14 +629,22 @@ def run_config4(args, rank, world, local):
     n_glob = n * world
     part = torch.empty(2, dtype=torch.float64, device="cuda")
     part2 = torch.empty(2, dtype=torch.float64, device="cuda")
-    res = torch.empty(2, dtype=torch.float64, device="cuda")
+    counts = D.shard_counts(n_glob, world, L)
+    tp = D.P2PTransport() if args.reduce_transport == "p2p" else None
+
+    def cross(p):  # the one exchange step: partials of every rank -> global twofold
+        if world == 1:
+            return
+        if tp is not None:
+            tp.combine(p, counts)  # NVLink mailboxes, no NCCL
+        else:
+            R.combine(D.gather_partials(p), counts, out=p)  # NCCL all-gather + tf_combine
 
     def step():
         R.vtdot(X, Y, out=part)
+        cross(part)
         R.vtsum(X, out=part2)
-        if world > 1:
-            allp = D.gather_partials(part)
-            R.combine(allp, D.shard_counts(n_glob, world, L), out=res)
+        cross(part2)
 
     for _ in range(args.warmup):
         step()
@@ -650,10 +661,9 @@ def run_config4(args, rank, world, local):
             ev[s][0].record(stream)
             R.vtdot(X, Y, out=part)
             ev[s][1].record(stream)
+            cross(part)
             R.vtsum(X, out=part2)
-            if world > 1:
-                allp = D.gather_partials(part)
-                R.combine(allp, D.shard_counts(n_glob, world, L), out=res)
+            cross(part2)
         end.record(stream)
         torch.cuda.synchronize()
     barrier(world)
@@ -687,7 +697,8 @@ def run_config4(args, rank, world, local):
             "e2e": {"value": world * 2 * n * args.e2e_steps / dt, "unit": "elem-ops/s",
                     "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 32,
                     "path": "reduce.vtdot / vtsum on pinned numpy planes -> tf_reduce_host"},
-            "gpu_launches": world * K * (2 + (1 if world > 1 else 0)),
+            "gpu_launches": world * K * (2 + (2 if world > 1 else 0)),
+            "reduce_transport": args.reduce_transport if world > 1 else "none (1 GPU)",
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
