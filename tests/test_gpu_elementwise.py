@@ -360,3 +360,39 @@ def test_all_ops_on_random_bit_patterns(oracle, fmt):
         r0, r1 = run_device(name, ins)
         assert bits_equal(r0, w0), (name, first_mismatch(r0, w0))
         assert bits_equal(r1, w1), (name, first_mismatch(r1, w1))
+
+
+def test_cuda_graph_capture_and_replay(oracle):
+    # the launchers are CUDA-graph safe: a captured step of several ops (and a
+    # reduction) replays with the same bits as eager execution
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+
+    n = (1 << 20) + 3
+    ins = _config2_inputs("vtdiv2", n, 91)
+    X = K.TwofoldArray(_t(ins[0]), _t(ins[1]))
+    Y = K.TwofoldArray(_t(ins[2]), _t(ins[3]))
+    o1, o2 = K.empty_twofold(n, torch.float64), K.empty_twofold(n, torch.float64)
+    red = torch.empty(2, dtype=torch.float64, device=DEV)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):  # warm (self-test, occupancy, workspace) outside capture
+        K.vtdiv2(X, Y, o1)
+        K.vtadd2(o1, Y, o2)
+        R.vtdot(o2.value, Y.value, out=red)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        K.vtdiv2(X, Y, o1)
+        K.vtadd2(o1, Y, o2)
+        R.vtdot(o2.value, Y.value, out=red)
+    for buf in (o1.value, o1.error, o2.value, o2.error, red):
+        buf.fill_(7.0)
+    g.replay()
+    g.replay()
+    torch.cuda.synchronize()
+    w1 = oracle.elementwise("vtdiv2", *ins)
+    w2 = oracle.elementwise("vtadd2", w1[0], w1[1], ins[2], ins[3])
+    assert bits_equal(o1.value.cpu().numpy(), w1[0]) and bits_equal(o1.error.cpu().numpy(), w1[1])
+    assert bits_equal(o2.value.cpu().numpy(), w2[0]) and bits_equal(o2.error.cpu().numpy(), w2[1])
+    wr = oracle.reduce("dot", w2[0], ins[2], geometry=R.geometry(np.float64))
+    assert (red[0].item(), red[1].item()) == (float(wr[0]), float(wr[1]))
