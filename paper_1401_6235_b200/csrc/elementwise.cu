@@ -18,6 +18,7 @@
 // TF_EW_SCHED=persistent select the earlier variants for A/B measurements.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -117,14 +118,14 @@ struct EwEntry {
   const void* fn;  // kernel symbol
   int nin;
   int unroll;
-  int max_blocks_per_sm;  // occupancy, filled lazily
+  std::atomic<int> max_blocks_per_sm;  // occupancy, filled lazily (idempotent)
 };
 
 template <class T, int OP, int VB>
 EwEntry make_entry() {
   constexpr int NIN = OpInfo<OP>::NIN;
   constexpr int U = (VB == 32) ? (NIN >= 3 ? 1 : 2) : Unroll<NIN>::U;
-  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>), NIN, U, 0};
+  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>), NIN, U, {0}};
 }
 
 template <class T, int VB, int... OPS>
@@ -145,11 +146,10 @@ static EwEntry* table_for(int dtype, int vb) {
 // vector width of the split-layout body: 32-byte (sm_100 256-bit LDG/STG) by
 // default; TF_VEC_BYTES=16 selects the 128-bit variant (A/B measurements)
 static int vec_bytes() {
-  static int vb = 0;
-  if (!vb) {
+  static const int vb = [] {  // thread-safe one-time init
     const char* e = getenv("TF_VEC_BYTES");
-    vb = (e && atoi(e) == 16) ? 16 : 32;
-  }
+    return (e && atoi(e) == 16) ? 16 : 32;
+  }();
   return vb;
 }
 
@@ -191,22 +191,23 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     nvec = 0;
   }
 
-  if (ent.max_blocks_per_sm == 0) {
+  int mbs = ent.max_blocks_per_sm.load(std::memory_order_relaxed);
+  if (mbs == 0) {
     int b = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, ent.fn, 256, 0);
     if (e != cudaSuccess) return cuda_status(e, "tf_elementwise: occupancy");
-    ent.max_blocks_per_sm = b > 0 ? b : 1;
+    mbs = b > 0 ? b : 1;
+    ent.max_blocks_per_sm.store(mbs, std::memory_order_relaxed);
   }
   // one CTA per chunk of 256*U*4 vectors (hardware-balanced); TF_EW_SCHED=
   // persistent caps the grid at the resident CTAs instead (A/B measurements)
   const int64_t chunk = 256LL * ent.unroll * 4;
   int64_t blocks = nvec > 0 ? (nvec + chunk - 1) / chunk : (n + 255) / 256;
-  const int64_t resident = (int64_t)sm_count() * ent.max_blocks_per_sm;
-  static int persistent = -1;
-  if (persistent < 0) {
+  const int64_t resident = (int64_t)sm_count() * mbs;
+  static const bool persistent = [] {
     const char* e = getenv("TF_EW_SCHED");
-    persistent = (e && e[0] == 'p') ? 1 : 0;
-  }
+    return e && e[0] == 'p';
+  }();
   const int64_t cap = persistent || nvec == 0 ? resident : (int64_t)0x7fffffff;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;

@@ -180,12 +180,11 @@ __global__ void __launch_bounds__(256) deinterleave_kernel(const T* __restrict__
 
 struct IlEntry {
   const void* fn;
-  int occ;
 };
 
 template <class T, int OP>
 IlEntry make_il() {
-  return IlEntry{reinterpret_cast<const void*>(&ew_il_kernel<T, OP>), 0};
+  return IlEntry{reinterpret_cast<const void*>(&ew_il_kernel<T, OP>)};
 }
 template <class T, int... OPS>
 struct IlTable {
@@ -204,8 +203,7 @@ static IlEntry* il_table(int dtype) {
 
 // one CTA per 256 work items: the hardware block scheduler balances the SMs
 // (a grid capped at the resident CTAs leaves a tail of idle SMs, -6% on B200)
-static int64_t grid_for(int64_t work, int occ) {
-  (void)occ;
+static int64_t grid_for(int64_t work) {
   int64_t blocks = (work + 255) / 256;
   if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;
   return blocks < 1 ? 1 : blocks;
@@ -222,13 +220,7 @@ int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* 
                                          2, 1, 4, 4, 4, 4, 3, 3, 3, 3, 2, 1};
   const bool binary = nin_of[op] >= 2 && op != TF_VTSQRT1;
   if (!a || !out || (binary && !b)) return fail(TF_EINVAL, "tf_elementwise_il: null array");
-  IlEntry& ent = il_table(dtype)[op];
-  if (!ent.occ) {
-    int o = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, ent.fn, 256, 0);
-    if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_il: occupancy");
-    ent.occ = o > 0 ? o : 1;
-  }
+  const IlEntry& ent = il_table(dtype)[op];
   // pair arrays need 32-byte alignment, plain planes 16-byte
   const int ar = nin_of[op] == 4 ? 22 : nin_of[op] == 3 ? 21 : op == TF_VTSQRT1 ? 2 : nin_of[op] == 2 ? 11 : 1;
   const bool xpairs = ar == 22 || ar == 21 || ar == 2;
@@ -237,7 +229,7 @@ int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* 
   const int E = dtype == TF_F64 ? 2 : 4;
   ILArgs<double> p{static_cast<const double*>(a), static_cast<const double*>(b ? b : a),
                    static_cast<double*>(out)};
-  const int64_t blocks = grid_for(vec ? (n / E + 1) / 2 : n, ent.occ);
+  const int64_t blocks = grid_for(vec ? (n / E + 1) / 2 : n);
   void* args[] = {&p, &n, &vec};
   return cuda_status(cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, s),
                      "tf_elementwise_il: launch");
@@ -252,7 +244,7 @@ int convert_launch(int to_interleaved, int dtype, int64_t n, const void* a, cons
   if (to_interleaved) {  // a = value, b = error, c = pairs
     if (!a || !b || !c) return fail(TF_EINVAL, "tf_interleave: null array");
     int vec = aligned16(a) && aligned16(b) && aligned16(c);
-    const int64_t blocks = grid_for(vec ? n / E : n, 8);
+    const int64_t blocks = grid_for(vec ? n / E : n);
     if (dtype == TF_F64)
       interleave_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
           (const double*)a, (const double*)b, (double*)c, n, vec);
@@ -262,7 +254,7 @@ int convert_launch(int to_interleaved, int dtype, int64_t n, const void* a, cons
   } else {  // a = pairs, b = value out, c = error out
     if (!a || !b || !c) return fail(TF_EINVAL, "tf_deinterleave: null array");
     int vec = aligned16(a) && aligned16(b) && aligned16(c);
-    const int64_t blocks = grid_for(vec ? n / E : n, 8);
+    const int64_t blocks = grid_for(vec ? n / E : n);
     if (dtype == TF_F64)
       deinterleave_kernel<double><<<(unsigned)blocks, 256, 0, s>>>(
           (const double*)a, (double*)const_cast<void*>(b), (double*)c, n, vec);

@@ -408,12 +408,11 @@ int reduce_geometry(int dtype, int* V, int* W, int* K) {
 // register path 7256 GB/s, bulk path 7191 GB/s); the register path is the
 // default, TF_REDUCE_PATH=bulk selects the TMA bulk-copy path.
 static bool use_bulk() {
-  static int v = -1;
-  if (v < 0) {
+  static const bool v = [] {  // thread-safe one-time init
     const char* e = getenv("TF_REDUCE_PATH");
-    v = (e && e[0] == 'b') ? 1 : 0;
-  }
-  return v == 1;
+    return e && e[0] == 'b';
+  }();
+  return v;
 }
 
 template <class T, int ROP>
@@ -427,14 +426,11 @@ static int reduce_t(int64_t n, const void* a, const void* b, void* out, void* ws
   const T* pb = static_cast<const T*>(b ? b : a);
   T* po = static_cast<T*>(out);
   if (vec && use_bulk()) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(reduce_bulk_kernel<T, ROP>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           BulkGeo<ROP>::SMEM);
-      if (e != cudaSuccess) return cuda_status(e, "tf_reduce: smem attribute");
-      attr = true;
-    }
+    // per call: the attribute is per device, and the call is cheap
+    cudaError_t e = cudaFuncSetAttribute(reduce_bulk_kernel<T, ROP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         BulkGeo<ROP>::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "tf_reduce: smem attribute");
     reduce_bulk_kernel<T, ROP><<<(unsigned)nt, RW, BulkGeo<ROP>::SMEM, s>>>(pa, pb, n, nt, tiles,
                                                                            counter, po);
   } else if (vec) {
