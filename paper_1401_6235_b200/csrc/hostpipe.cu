@@ -508,3 +508,28 @@ extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, cons
   cudaFree(parts);
   return rc;
 }
+
+// ---- page-locking of reused pageable planes ------------------------------------
+// Pageable planes cross the link through staging copies (host DRAM traffic x3);
+// registering a plane that is reused makes it DMA-able in place.  The Python
+// layer decides what to register (second use, size, budget) and unregisters it
+// before its memory is released.
+extern "C" int tf_host_register(void* ptr, size_t bytes) {
+  if (!ptr || !bytes) return fail(TF_EINVAL, "tf_host_register: bad arguments");
+  cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_status(e, "tf_host_register");
+  }
+  return TF_OK;
+}
+
+extern "C" int tf_host_unregister(void* ptr) {
+  if (!ptr) return fail(TF_EINVAL, "tf_host_unregister: null pointer");
+  cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return cuda_status(e, "tf_host_unregister");
+  }
+  return TF_OK;
+}

@@ -222,6 +222,9 @@ def _launch(name, op, planes, nin):
     else:
         dev = torch.cuda.current_device() if torch is not None else 0
         _lib.ensure_device(dev)
+        for p in planes:
+            if isinstance(p.obj, np.ndarray):
+                _maybe_register(p.obj)
         rc = L.tf_elementwise_host(op, _dtype_id(first.dtype), n, ins, outs, dev)
         _lib.check(rc, name)
 
@@ -363,6 +366,9 @@ def host_batch(calls, device=None):
         desc = _check(name, planes, (r0, r1))
         if any(d.kind != "host" for d in desc):
             raise ValueError("%s: host_batch takes numpy (host) planes" % name)
+        for d in desc:
+            if isinstance(d.obj, np.ndarray):
+                _maybe_register(d.obj)
         if first is None:
             first = desc[0]
         elif desc[0].dtype != first.dtype or desc[0].n != first.n:
@@ -379,3 +385,68 @@ def host_batch(calls, device=None):
     rc = L.tf_elementwise_host_batch(len(ops), arr_ops, _dtype_id(first.dtype), first.n,
                                      _lib.ptr_array(ins), _lib.ptr_array(outs), dev)
     _lib.check(rc, "host_batch")
+
+
+# --------------------------------------------------------------------------
+# page-locking of reused pageable numpy planes (host path)
+#
+# A pageable plane goes through pinned staging (three trips through host DRAM).
+# A plane seen a second time (the reference's loops reuse their arrays) is
+# page-locked in place with tf_host_register, within a byte budget (LRU), and
+# unregistered by a weakref finalizer before numpy releases its memory.
+
+import collections as _collections
+import os as _os
+import threading as _threading
+import weakref as _weakref
+
+_REG_LOCK = _threading.Lock()
+_REG = _collections.OrderedDict()  # owner address -> (nbytes, finalizer)
+_SEEN = {}
+_REG_MIN = 32 << 20
+_REG_BUDGET = int(float(_os.environ.get("TF_HOST_REGISTER_GB", "16")) * (1 << 30))
+
+
+def _owner(a):
+    o = a
+    while isinstance(o, np.ndarray) and o.base is not None:
+        o = o.base
+    if not isinstance(o, np.ndarray) or not o.flags.owndata:
+        return None  # memory owned elsewhere (torch pinned, mmap, ...): leave it alone
+    return o
+
+
+def _unregister(addr):
+    try:
+        (_lib._lib or _lib.lib()).tf_host_unregister(addr)
+    except Exception:  # pragma: no cover - interpreter shutdown
+        pass
+    with _REG_LOCK:
+        _REG.pop(addr, None)
+
+
+def _maybe_register(a):
+    if _REG_BUDGET <= 0:
+        return
+    o = _owner(a)
+    if o is None or o.nbytes < _REG_MIN:
+        return
+    addr = o.ctypes.data
+    with _REG_LOCK:
+        if addr in _REG:
+            _REG.move_to_end(addr)
+            return
+        _SEEN[addr] = _SEEN.get(addr, 0) + 1
+        if _SEEN[addr] < 2 or o.nbytes > _REG_BUDGET:
+            return
+        total = sum(v[0] for v in _REG.values())
+        while _REG and total + o.nbytes > _REG_BUDGET:
+            old, (nb, fin) = _REG.popitem(last=False)
+            fin.detach()
+            (_lib._lib or _lib.lib()).tf_host_unregister(old)
+            total -= nb
+        if (_lib._lib or _lib.lib()).tf_host_register(addr, o.nbytes) != 0:
+            _SEEN[addr] = -(1 << 30)  # not registrable: stay on the staging path
+            return
+        _REG[addr] = (o.nbytes, _weakref.finalize(o, _unregister, addr))
+        _SEEN.pop(addr, None)

@@ -80,6 +80,11 @@ def _reduce(name, rop, ins, out=None):
             raise ValueError("%s: out= is for CUDA planes" % name)
         dev = torch.cuda.current_device() if torch is not None else 0
         _lib.ensure_device(dev)
+        from .kernels import _maybe_register
+
+        for p in planes:
+            if isinstance(p.obj, np.ndarray):
+                _maybe_register(p.obj)
         dt = _dtype_id(first.dtype)
         res = np.zeros(2, first.dtype)
         rc = _lib.lib().tf_reduce_host(_lib.ROP_IDS[rop], dt, first.n, planes[0].ptr,

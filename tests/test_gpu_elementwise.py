@@ -396,3 +396,27 @@ def test_cuda_graph_capture_and_replay(oracle):
     assert bits_equal(o2.value.cpu().numpy(), w2[0]) and bits_equal(o2.error.cpu().numpy(), w2[1])
     wr = oracle.reduce("dot", w2[0], ins[2], geometry=R.geometry(np.float64))
     assert (red[0].item(), red[1].item()) == (float(wr[0]), float(wr[1]))
+
+
+def test_reused_pageable_planes_get_page_locked(oracle):
+    # second use of a large pageable numpy plane registers it (DMA in place);
+    # results stay bit-exact and the registration is released with the array
+    import gc
+
+    from paper_1401_6235_b200 import kernels as K
+
+    n = 5 << 20  # 40 MiB per f64 plane
+    ins = _config2_inputs("vtmul2", n, 5)
+    x = K.TwofoldArray(ins[0].copy(), ins[1].copy())
+    y = K.TwofoldArray(ins[2].copy(), ins[3].copy())
+    out = K.empty_twofold(n, np.float64, device="cpu")
+    w0, w1 = oracle.elementwise("vtmul2", *ins)
+    for _ in range(3):
+        out.value[:] = 7.0
+        K.vtmul2(x, y, out)
+        assert bits_equal(out.value, w0) and bits_equal(out.error, w1)
+    addrs = {a.ctypes.data for a in (x.value, x.error, y.value, y.error)}
+    assert addrs <= set(K._REG), "reused planes were not page-locked"
+    del x, y, out
+    gc.collect()
+    assert not (addrs & set(K._REG)), "registrations outlived their arrays"
