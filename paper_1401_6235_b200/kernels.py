@@ -391,9 +391,10 @@ def host_batch(calls, device=None):
 # page-locking of reused pageable numpy planes (host path)
 #
 # A pageable plane goes through pinned staging (three trips through host DRAM).
-# A plane seen a second time (the reference's loops reuse their arrays) is
-# page-locked in place with tf_host_register, within a byte budget (LRU), and
-# unregistered by a weakref finalizer before numpy releases its memory.
+# A plane seen TF_HOST_REGISTER_AFTER (4) times — the reference's loops reuse
+# their arrays — is page-locked in place with tf_host_register, within a byte
+# budget (LRU), and unregistered by a weakref finalizer before numpy releases
+# its memory.
 
 import collections as _collections
 import os as _os
@@ -405,6 +406,9 @@ _REG = _collections.OrderedDict()  # owner address -> (nbytes, finalizer)
 _SEEN = {}
 _REG_MIN = 32 << 20
 _REG_BUDGET = int(float(_os.environ.get("TF_HOST_REGISTER_GB", "16")) * (1 << 30))
+# page-locking costs ~80 ms per GiB (measured) and saves ~40% of a staged call,
+# so it pays for itself only on planes reused several times
+_REG_AFTER = int(_os.environ.get("TF_HOST_REGISTER_AFTER", "4"))
 
 
 def _owner(a):
@@ -437,7 +441,7 @@ def _maybe_register(a):
             _REG.move_to_end(addr)
             return
         _SEEN[addr] = _SEEN.get(addr, 0) + 1
-        if _SEEN[addr] < 2 or o.nbytes > _REG_BUDGET:
+        if _SEEN[addr] < _REG_AFTER or o.nbytes > _REG_BUDGET:
             return
         total = sum(v[0] for v in _REG.values())
         while _REG and total + o.nbytes > _REG_BUDGET:

@@ -411,7 +411,7 @@ def test_reused_pageable_planes_get_page_locked(oracle):
     y = K.TwofoldArray(ins[2].copy(), ins[3].copy())
     out = K.empty_twofold(n, np.float64, device="cpu")
     w0, w1 = oracle.elementwise("vtmul2", *ins)
-    for _ in range(3):
+    for _ in range(K._REG_AFTER + 1):
         out.value[:] = 7.0
         K.vtmul2(x, y, out)
         assert bits_equal(out.value, w0) and bits_equal(out.error, w1)
