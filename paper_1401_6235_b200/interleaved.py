@@ -14,10 +14,9 @@ planes.  Same names, arities, numerics (bit for bit) and validation rules as
 
 from __future__ import annotations
 
-import numpy as np
 
 from . import _lib
-from .kernels import _TABLE, RAW_OPS, CoupledArray, TwofoldArray
+from .kernels import _TABLE, RAW_OPS, TwofoldArray
 
 try:
     import torch

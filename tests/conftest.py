@@ -4,7 +4,6 @@ Markers: ``gpu`` tests need a B200 (run via gpurun / the driver's GPU tier);
 everything else runs on the CPU-only build container.
 """
 
-import os
 import sys
 from pathlib import Path
 

@@ -10,7 +10,6 @@ inputs, so the comparison is bit-for-bit on every element.
 import hashlib
 import json
 import sys
-from pathlib import Path
 
 import numpy as np
 import pytest

@@ -1,5 +1,5 @@
 """Host<->device link probe and e2e pipeline sweep (run on the GPU box)."""
-import os, subprocess, sys, time, json
+import os, sys, time, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 

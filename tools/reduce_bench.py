@@ -1,7 +1,6 @@
 """Reduction and Horner throughput, f32 and f64 (CUDA-graph repeat loops)."""
 import json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import torch
 from paper_1401_6235_b200 import reduce as R, kernels as K, workloads as W
 from paper_1401_6235_b200.gpubench import _measure, _peak_gbs
