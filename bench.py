@@ -595,6 +595,8 @@ def run_elementwise(args, rank, world, local):
                        "l2_flush": "512 MB memset between steps (outside the timed intervals)"
                        if flush else None,
                        "layout": "split SoA planes",
+                       "inputs": "tf_fill counter-based splitmix64 on the device; plane k seed "
+                                 "1000+17k, element i of rank r is global index r*n+i",
                        "l2": ("working set %d MiB < L2 x3: flushed" if flush else
                               "working set %d MiB >> 126 MB L2; no flush") % (ws_bytes >> 20)},
             "hbm_gbs": world * bytes_per_step * K / (elapsed_ms * 1e-3) / 1e9,
