@@ -292,3 +292,47 @@ def test_p2p_transport_single_rank_matches_combine():
         tp.combine(part32, [n])
         assert (part32[0].item(), part32[1].item()) == (w32.value, w32.error)
     assert tp.status() == 0
+
+
+def test_concurrent_threads_and_streams(oracle):
+    # four Python threads, each on its own CUDA stream, run elementwise ops,
+    # reductions (per-stream workspaces) and host-plane calls (per-device pipe
+    # lock) at the same time; every result must still be bit-exact
+    import threading
+
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+
+    n = (1 << 21) + 7
+    errors = []
+
+    def work(seed):
+        try:
+            rng = np.random.default_rng(seed)
+            x = rng.uniform(-1, 1, n)
+            y = rng.uniform(-1, 1, n)
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                X, Y = _t(x), _t(y)
+                for _ in range(3):
+                    out = K.empty_twofold(n, torch.float64)
+                    K.vtmul2(K.TwofoldArray(X, Y), K.TwofoldArray(Y, X), out)
+                    z = R.vtdot(X, Y)
+                    s.synchronize()
+                    w = oracle.elementwise("vtmul2", x, y, y, x)
+                    assert np.array_equal(out.value.cpu().numpy().view(np.uint64), w[0].view(np.uint64))
+                    wd = oracle.reduce("dot", x, y, geometry=_geom(np.float64))
+                    assert (z.value, z.error) == (float(wd[0]), float(wd[1]))
+                    oh = K.empty_twofold(n, np.float64, device="cpu")
+                    K.vtadd2(K.TwofoldArray(x, y), K.TwofoldArray(y, x), oh)
+                    wa = oracle.elementwise("vtadd2", x, y, y, x)
+                    assert np.array_equal(oh.value.view(np.uint64), wa[0].view(np.uint64))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
