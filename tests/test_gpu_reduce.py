@@ -231,20 +231,22 @@ def test_horner_generic_degree_vs_oracle(oracle):
     assert np.array_equal(out.error.cpu().numpy().view(np.uint64), w1.view(np.uint64))
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("pin", [False, True])
 @pytest.mark.parametrize("rop", ["sum", "sum2", "dot"])
-def test_host_plane_reductions_match_device(oracle, rop, pin):
+def test_host_plane_reductions_match_device(oracle, rop, pin, dtype):
     # numpy planes go through tf_reduce_host (chunked subtrees + combine): the
     # bits must equal the device-plane reduction and the oracle
     from paper_1401_6235_b200 import reduce as R
 
     rng = np.random.default_rng(99)
     n = 37 * 65536 + 12345  # several pipeline chunks plus a partial tile
-    x = rng.uniform(-1, 1, n) * np.exp2(rng.integers(-30, 31, n))
-    y = rng.uniform(-1, 1, n)
+    x = (rng.uniform(-1, 1, n) * np.exp2(rng.integers(-30, 31, n))).astype(dtype)
+    y = rng.uniform(-1, 1, n).astype(dtype)
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
     if pin:
-        xp = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
-        yp = torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+        xp = torch.empty(n, dtype=tdt, pin_memory=True).numpy()
+        yp = torch.empty(n, dtype=tdt, pin_memory=True).numpy()
         xp[:] = x
         yp[:] = y
         x, y = xp, yp
@@ -252,7 +254,7 @@ def test_host_plane_reductions_match_device(oracle, rop, pin):
           "dot": lambda a, b: R.vtdot(a, b)}[rop]
     zh = fn(x, y)
     zd = fn(_t(x), _t(y))
-    w = oracle.reduce(rop, x, None if rop == "sum" else y, geometry=_geom(np.float64))
+    w = oracle.reduce(rop, x, None if rop == "sum" else y, geometry=_geom(dtype))
     assert (zh.value, zh.error) == (zd.value, zd.error) == (float(w[0]), float(w[1]))
 
 
