@@ -48,9 +48,10 @@ __device__ __forceinline__ P<T> xcomb(P<T> l, P<T> r) {
   return tadd(l.a, l.b, r.a, r.b);
 }
 
+// The protocol, for one rank; run by one thread.  Shared by the real transport
+// kernel (one rank per GPU) and the one-GPU emulation (one rank per block).
 template <class T>
-__global__ void xgpu_exchange_kernel(T* out, XArgs x, int* status) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ void xgpu_exchange(T* out, const XArgs& x, int* status) {
   const int par = (int)(x.epoch & 1);
   const volatile T* mine_v = out;
   const double z0 = (double)mine_v[0], z1 = (double)mine_v[1];
@@ -106,6 +107,31 @@ __global__ void xgpu_exchange_kernel(T* out, XArgs x, int* status) {
   for (int s = sp - 2; s >= 0; s--) acc = xcomb(st[s], acc);
   out[0] = acc.a;
   out[1] = acc.b;
+}
+
+template <class T>
+__global__ void xgpu_exchange_kernel(T* out, XArgs x, int* status) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  xgpu_exchange(out, x, status);
+}
+
+// One-GPU emulation of `world` ranks: block r plays rank r over mailboxes that
+// all live in this GPU's memory, for `epochs` back-to-back exchanges (both
+// parity buffers).  All blocks of one small grid are co-resident, so the spin
+// waits between them are safe on one device (unlike separate launches).
+template <class T>
+__global__ void xgpu_emulate_kernel(T* io, XArgs base, int epochs, int* status) {
+  if (threadIdx.x != 0) return;
+  XArgs x = base;
+  x.rank = blockIdx.x;
+  T* out = io + 2 * blockIdx.x;
+  const T p0 = out[0], p1 = out[1];
+  for (int e = 0; e < epochs; e++) {
+    out[0] = p0;  // every epoch starts from this rank's own partial
+    out[1] = p1;
+    x.epoch = base.epoch + e;
+    xgpu_exchange(out, x, status);
+  }
 }
 
 struct XCtx {
@@ -209,4 +235,46 @@ extern "C" int tf_xgpu_status(int device) {
   int v = 0;
   cudaMemcpy(&v, c->status, sizeof v, cudaMemcpyDeviceToHost);
   return v;
+}
+
+// Test entry: emulate `world` ranks on this GPU.  io (device, world x 2 of dtype)
+// holds each rank's partial on entry and each rank's combined result on exit.
+extern "C" int tf_xgpu_emulate(int dtype, int world, void* io, const int64_t* counts,
+                               int epochs, void* stream) {
+  if ((dtype != TF_F32 && dtype != TF_F64) || world < 1 || world > XG_MAXG || !io || !counts ||
+      epochs < 1)
+    return fail(TF_EINVAL, "tf_xgpu_emulate: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Slot* boxes = nullptr;
+  int* status = nullptr;
+  const size_t bytes = sizeof(Slot) * 2 * XG_MAXG * world;
+  cudaError_t e = cudaMalloc(&boxes, bytes);
+  if (e == cudaSuccess) e = cudaMemset(boxes, 0xff, bytes);
+  if (e == cudaSuccess) e = cudaMalloc(&status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(status, 0, sizeof(int));
+  if (e != cudaSuccess) return cuda_status(e, "tf_xgpu_emulate");
+  XArgs x{};
+  for (int r = 0; r < world; r++) x.box[r] = boxes + (size_t)r * 2 * XG_MAXG;
+  x.world = world;
+  x.epoch = 1;
+  for (int r = 0; r < world; r++)
+    if (counts[r] > 0) {
+      if (r < 32) x.nonempty_lo |= 1ull << r;
+      else x.nonempty_hi |= 1ull << (r - 32);
+    }
+  if (dtype == TF_F64)
+    xgpu_emulate_kernel<double><<<world, 32, 0, s>>>(static_cast<double*>(io), x, epochs, status);
+  else
+    xgpu_emulate_kernel<float><<<world, 32, 0, s>>>(static_cast<float*>(io), x, epochs, status);
+  int rc = launch_status("tf_xgpu_emulate");
+  int h = 0;
+  if (!rc) {
+    e = cudaMemcpyAsync(&h, status, sizeof h, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_status(e, "tf_xgpu_emulate");
+  }
+  cudaFree(boxes);
+  cudaFree(status);
+  if (!rc && h) rc = fail(TF_ECUDA, "tf_xgpu_emulate: exchange timed out");
+  return rc;
 }

@@ -296,6 +296,40 @@ def test_p2p_transport_single_rank_matches_combine():
     assert tp.status() == 0
 
 
+@pytest.mark.parametrize("world", [2, 3, 5, 8, 13, 64])
+@pytest.mark.parametrize("tdt", [torch.float64, torch.float32])
+def test_p2p_protocol_emulated_ranks_match_combine(world, tdt):
+    # the multi-rank mailbox protocol of csrc/xgpu.cu (publish to every peer,
+    # system fence, epoch flags, bounded wait, skip-tree fold) with every rank
+    # played by one block of a single kernel on this GPU, over 6 epochs (both
+    # parity buffers, each reused): every rank must end with exactly the
+    # tf_combine result, empty shards skipped as tf_combine skips them
+    import ctypes
+
+    from paper_1401_6235_b200 import _lib
+    from paper_1401_6235_b200 import reduce as R
+
+    rng = np.random.default_rng(world)
+    parts = []
+    for r in range(world):
+        x = _t(rng.uniform(-1, 1, 70000) * np.exp2(rng.integers(-30, 31, 70000))).to(tdt)
+        p = torch.empty(2, dtype=tdt, device=DEV)
+        R.vtsum(x, out=p)
+        parts.append(p)
+    P = torch.stack(parts)
+    counts = [0 if (r % 4 == 1) else 70000 for r in range(world)]
+    want = R.combine(P, counts)
+    io = P.clone().contiguous()
+    dt = _lib.TF_F64 if tdt == torch.float64 else _lib.TF_F32
+    c = (ctypes.c_int64 * world)(*counts)
+    stream = torch.cuda.current_stream().cuda_stream
+    rc = _lib.lib().tf_xgpu_emulate(dt, world, io.data_ptr(), c, 6, stream)
+    _lib.check(rc, "tf_xgpu_emulate")
+    got = io.cpu().tolist()
+    for r in range(world):
+        assert (got[r][0], got[r][1]) == (want.value, want.error), (r, got[r], want)
+
+
 def test_concurrent_threads_and_streams(oracle):
     # four Python threads, each on its own CUDA stream, run elementwise ops,
     # reductions (per-stream workspaces) and host-plane calls (per-device pipe
