@@ -320,6 +320,40 @@ def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3, pla
     return total_units / t_total, nt, planes
 
 
+def _best_of(fn, reps=3):
+    fn()  # warm-up (thread pool, page faults)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best
+
+
+def cpu_baseline_reduce(xh, yh, n_sample, reps=3):
+    """Oracle canonical-order vtdot + vtsum (C, OpenMP over tiles, all host
+    threads) on the first n_sample elements of the bench's own host planes."""
+    from oracle import oracle as o
+
+    nt = os.cpu_count() or 1
+    xs, ys = xh[:n_sample], yh[:n_sample]
+    t_dot = _best_of(lambda: o.reduce("dot", xs, ys, geometry=(2, 256, 128), nthreads=nt), reps)
+    t_sum = _best_of(lambda: o.reduce("sum", xs, geometry=(2, 256, 128), nthreads=nt), reps)
+    return 2 * n_sample / (t_dot + t_sum), nt
+
+
+def cpu_baseline_horner(xh, coeffs, n_sample, reps=3):
+    """Oracle twofold Horner (C, OpenMP, all host threads) on a bounded sample."""
+    from oracle import oracle as o
+
+    nt = os.cpu_count() or 1
+    xs = xh[:n_sample]
+    out = (np.zeros_like(xs), np.zeros_like(xs))
+    t = _best_of(lambda: o.horner(coeffs, xs, nthreads=nt, out=out), reps)
+    return n_sample / t, nt
+
+
 def host_dists(workload):
     """numpy generators with the same distributions as the device fill (CPU arms)."""
 
@@ -372,6 +406,10 @@ def run_reference(args, rank, world):
     """CPU reference arm: the oracle port on all host threads (rank 0 only)."""
     if rank != 0:
         return 0
+    if args.workload == "config4":
+        return run_reference_config4(args)
+    if args.workload == "config5":
+        return run_reference_config5(args)
     wl = WL.get(args.workload, WL["config2"])
     n_sample = min(args.n or wl["n"], args.cpu_sample, 1 << 25)
     from oracle import oracle as o
@@ -412,6 +450,79 @@ def run_reference(args, rank, world):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _reference_line(args, metric, value, unit, dtype, workload, sample, nt, **extra):
+    line = {
+        "impl": "reference", "metric": metric, "value": value, "unit": unit,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
+        "config": {"workload": workload},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": nt, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    line.update(extra)
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _timed_steps(args, step):
+    for _ in range(max(args.warmup, 1)):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    return time.perf_counter() - t0
+
+
+def run_reference_config4(args):
+    """Reference arm for config4: oracle vtdot + vtsum in the canonical order on
+    all host threads, over a bounded sample of the ORO-style generator's planes
+    (generated untimed by the host-side generator, no device involved)."""
+    from oracle import oracle as o
+
+    import ctypes
+
+    from paper_1401_6235_b200 import _lib
+
+    ns = min(args.n or (1 << 30), args.cpu_sample, 1 << 25)
+    x, y = np.empty(ns), np.empty(ns)
+    _lib.check(_lib.lib().tf_gen_dot_host(ns, ctypes.c_double(1e16), 4242, x.ctypes.data,
+                                          y.ctypes.data), "tf_gen_dot_host")
+    nt = os.cpu_count() or 1
+
+    def step():
+        o.reduce("dot", x, y, geometry=(2, 256, 128), nthreads=nt)
+        o.reduce("sum", x, geometry=(2, 256, 128), nthreads=nt)
+
+    dt = _timed_steps(args, step)
+    value = 2 * ns * args.steps / dt
+    return _reference_line(
+        args, METRIC + " [config4: vtdot+vtsum]", value, "elem-ops/s", "f64",
+        "BASELINE configs[3]: f64 vtdot + vtsum, n=2^30 per GPU",
+        "%d-element ORO-style dot planes per step (vtdot + vtsum), oracle/twofold_oracle.c "
+        "canonical order, OpenMP over tiles" % ns, nt, ms_per_step=1e3 * dt / args.steps,
+        data="synthetic (ORO-style ill-conditioned dot, cond 1e16, seeded)")
+
+
+def run_reference_config5(args):
+    """Reference arm for config5: oracle twofold Horner of (x-1)^20, all host threads."""
+    from oracle import oracle as o
+
+    ns = min(args.n or (1 << 26), args.cpu_sample, 1 << 24)
+    x = np.random.default_rng(555).uniform(0.9, 1.1, ns)
+    c = [float((-1) ** (20 - k) * __import__("math").comb(20, k)) for k in range(21)]
+    nt = os.cpu_count() or 1
+    out = (np.zeros_like(x), np.zeros_like(x))
+    dt = _timed_steps(args, lambda: o.horner(c, x, nthreads=nt, out=out))
+    value = ns * args.steps / dt
+    return _reference_line(
+        args, "twofold Horner points/s (fp64, (x-1)^20)", value, "points/s", "f64",
+        "BASELINE configs[4]: twofold Horner (x-1)^20, n=2^26 per GPU",
+        "%d points x ~ U[0.9,1.1] per step, oracle/twofold_oracle.c OpenMP" % ns, nt,
+        ms_per_step=1e3 * dt / args.steps, data="synthetic x ~ U[0.9,1.1] (seeded numpy)")
 
 
 def run_elementwise(args, rank, world, local):
@@ -684,6 +795,14 @@ def run_config4(args, rank, world, local):
         z2 = R.vtsum(xh)
     dt = max_over_ranks(time.perf_counter() - t0, world)
     del z, z2
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ns = min(n, args.cpu_sample)
+        v, nt = cpu_baseline_reduce(xh, yh, ns)
+        cpu = {"value": v, "unit": "elem-ops/s", "cores": nt, "kind": "port",
+               "sample": "first %d elements of the bench's own planes, vtdot + vtsum (best of 3 "
+                         "each), oracle/twofold_oracle.c canonical order, OpenMP on %d threads"
+                         % (ns, nt)}
     if rank == 0:
         gbs = 16 * n / (dot_ms * 1e-3) / 1e9
         line = {
@@ -699,6 +818,7 @@ def run_config4(args, rank, world, local):
             "e2e": {"value": world * 2 * n * args.e2e_steps / dt, "unit": "elem-ops/s",
                     "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 32,
                     "path": "reduce.vtdot / vtsum on pinned numpy planes -> tf_reduce_host"},
+            "cpu_baseline": cpu,
             "gpu_launches": world * K * (2 + (2 if world > 1 else 0)),
             "reduce_transport": args.reduce_transport if world > 1 else "none (1 GPU)",
             "clocks": clk.summary(),
@@ -756,6 +876,13 @@ def run_config5(args, rank, world, local):
     for _ in range(args.e2e_steps):
         R.vthorner(c, xh, oh)
     dte = max_over_ranks(time.perf_counter() - t0, world)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ns = min(ne, args.cpu_sample, 1 << 24)
+        v, nt = cpu_baseline_horner(xh, c, ns)
+        cpu = {"value": v, "unit": "points/s", "cores": nt, "kind": "port",
+               "sample": "first %d of the bench's own points (best of 3), oracle/twofold_oracle.c "
+                         "OpenMP on %d threads" % (ns, nt)}
     if rank == 0:
         line = {
             "metric": "twofold Horner points/s (fp64, (x-1)^20)", "value": value, "unit": "points/s",
@@ -773,6 +900,7 @@ def run_config5(args, rank, world, local):
                     "h2d_bytes_per_step": 8 * ne, "d2h_bytes_per_step": 16 * ne,
                     "elems_per_step": ne,
                     "path": "reduce.vthorner on pinned numpy planes -> tf_horner_host"},
+            "cpu_baseline": cpu,
             "gpu_launches": world * K,
             "clocks": clk.summary(),
         }

@@ -424,10 +424,29 @@ int tfo_horner(int dtype, int64_t n, const void* x_, const double* c, int degree
                void* o0_, void* o1_, int nthreads) {
   if (n < 0 || degree < 0) return -1;
   int nt = clamp_threads(nthreads);
+  /* Points are independent: blocks of HB points run the same per-point chain
+     side by side (lane loop innermost, so it vectorises); every point still
+     sees exactly the scalar sequence of operations, hence the same bits. */
+#define HB 16
 #define HORNER(S, T)                                                           \
   { const T* x = x_; T *o0 = o0_, *o1 = o1_;                                   \
+    const int64_t nb = n / HB;                                                 \
     _Pragma("omp parallel for schedule(static) num_threads(nt)")              \
-    for (int64_t i = 0; i < n; i++) {                                          \
+    for (int64_t blk = 0; blk < nb; blk++) {                                   \
+      const int64_t i0 = blk * HB;                                             \
+      T a[HB], b[HB];                                                          \
+      for (int j = 0; j < HB; j++) { a[j] = (T)c[degree]; b[j] = (T)0; }       \
+      for (int k = degree - 1; k >= 0; k--) {                                  \
+        const T ck = (T)c[k];                                                  \
+        for (int j = 0; j < HB; j++) {                                         \
+          pair_##S r = tmul1_##S(a[j], b[j], x[i0 + j]);                       \
+          r = tadd1_##S(r.a, r.b, ck);                                         \
+          a[j] = r.a; b[j] = r.b;                                              \
+        }                                                                      \
+      }                                                                        \
+      for (int j = 0; j < HB; j++) { o0[i0 + j] = a[j]; o1[i0 + j] = b[j]; }   \
+    }                                                                          \
+    for (int64_t i = nb * HB; i < n; i++) {                                    \
       pair_##S r = mk_##S((T)c[degree], (T)0);                                 \
       for (int k = degree - 1; k >= 0; k--) {                                  \
         r = tmul1_##S(r.a, r.b, x[i]);                                         \
@@ -439,6 +458,7 @@ int tfo_horner(int dtype, int64_t n, const void* x_, const double* c, int degree
   if (dtype == TF_F64) HORNER(d, double)
   if (dtype == TF_F32) HORNER(f, float)
 #undef HORNER
+#undef HB
   return -1;
 }
 

@@ -9,9 +9,14 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def test_reference_arm_json_line():
+import pytest
+
+
+@pytest.mark.parametrize("workload", ["config2", "config4", "config5"])
+def test_reference_arm_json_line(workload):
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
-                        "--steps", "2", "--warmup", "1", "--cpu-sample", "65536"],
+                        "--workload", workload, "--steps", "2", "--warmup", "1",
+                        "--cpu-sample", "65536"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
@@ -25,6 +30,7 @@ def test_reference_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+    assert ("configs[%d]" % {"config2": 1, "config4": 3, "config5": 4}[workload]) in d["config"]["workload"]
 
 
 def test_reference_arm_non_zero_ranks_exit_quietly():
