@@ -795,6 +795,13 @@ def run_config4(args, rank, world, local):
         z2 = R.vtsum(xh)
     dt = max_over_ranks(time.perf_counter() - t0, world)
     del z, z2
+    # the same step as ONE host pass (reduce.host_batch): x crosses the link once
+    R.host_batch([("vtdot", xh, yh), ("vtsum", xh)])
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        R.host_batch([("vtdot", xh, yh), ("vtsum", xh)])
+    dtb = max_over_ranks(time.perf_counter() - t0, world)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         ns = min(n, args.cpu_sample)
@@ -817,7 +824,11 @@ def run_config4(args, rank, world, local):
                          "algorithmic_bytes": 16 * n, "peak_source": src},
             "e2e": {"value": world * 2 * n * args.e2e_steps / dt, "unit": "elem-ops/s",
                     "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 32,
-                    "path": "reduce.vtdot / vtsum on pinned numpy planes -> tf_reduce_host"},
+                    "path": "reduce.vtdot / vtsum on pinned numpy planes -> tf_reduce_host",
+                    "batched": {"value": world * 2 * n * args.e2e_steps / dtb,
+                                "path": "reduce.host_batch([vtdot(x, y), vtsum(x)]): one pass, "
+                                        "x crosses the link once (tf_reduce_host_batch)",
+                                "h2d_bytes_per_step": 16 * n}},
             "cpu_baseline": cpu,
             "gpu_launches": world * K * (2 + (2 if world > 1 else 0)),
             "reduce_transport": args.reduce_transport if world > 1 else "none (1 GPU)",

@@ -368,42 +368,73 @@ int reduce_launch(int rop, int dtype, int64_t n, const void* a, const void* b, v
 int combine_launch(int dtype, int g, const void* partials, const int64_t* counts, void* out,
                    cudaStream_t s);
 
-struct RedStage {
+constexpr int RED_MAX_BATCH = 16;
+
+struct RedStage {  // per device: staging planes per slot (grown on demand)
   int64_t plane_bytes = 0;
-  void* d[HostPipe::MAX_SLOTS][2] = {};
-  void* h[HostPipe::MAX_SLOTS][2] = {};
-  void* ws[HostPipe::MAX_SLOTS] = {};
+  std::vector<void*> d[HostPipe::MAX_SLOTS];  // device planes
+  std::vector<void*> h[HostPipe::MAX_SLOTS];  // pinned staging (pageable inputs)
+  void* ws[HostPipe::MAX_SLOTS] = {};         // one per slot: its reductions run in order
   size_t ws_bytes = 0;
 };
 static RedStage g_red[64];
-}  // namespace tf
 
-// Reduce n elements of HOST planes (numpy) in the canonical order: chunks of C
-// tiles (C a power of two, so each chunk is a complete subtree of the tile tree)
-// stream through the slots; each chunk's subtree value lands in a device array
-// and the combine kernel folds them with the same adjacent-pair tree — the
-// result is bit-identical to tf_reduce on device planes.  Synchronous; writes
-// out[0..1] (host, dtype).
-extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, const void* b,
-                              void* out, int device) {
-  const char* who = "tf_reduce_host";
-  if (rop < 0 || rop >= TF_NUM_ROPS) return fail(TF_EINVAL, "tf_reduce_host: unknown reduction id");
+static void red_free(RedStage& R) {
+  for (int s = 0; s < HostPipe::MAX_SLOTS; s++) {
+    for (void* d : R.d[s]) cudaFree(d);
+    for (void* h : R.h[s]) cudaFreeHost(h);
+    R.d[s].clear();
+    R.h[s].clear();
+    if (R.ws[s]) cudaFree(R.ws[s]);
+    R.ws[s] = nullptr;
+  }
+  R.plane_bytes = 0;
+  R.ws_bytes = 0;
+}
+
+// Reduce n elements of HOST planes in the canonical order, `nred` reductions in
+// one pass: chunks of C tiles (C a power of two, so every chunk is a complete
+// subtree of the tile tree) stream through the slots; each distinct input plane
+// crosses the host link once per chunk however many reductions read it; each
+// chunk's subtree value lands in a device array and the combine kernel folds
+// them with the same adjacent-pair tree — every result is bit-identical to
+// tf_reduce on device planes.  Synchronous; writes out[2r..2r+1] (host, dtype).
+static int reduce_host_batch(int nred, const int* rops, int dtype, int64_t n,
+                             const void* const* a, const void* const* b, void* out,
+                             int device, const char* who) {
+  const std::string w(who);
+  if (nred < 1 || nred > RED_MAX_BATCH) return fail(TF_EINVAL, w + ": 1..16 reductions per batch");
   if (dtype != TF_F32 && dtype != TF_F64)
-    return fail(TF_EINVAL, "tf_reduce_host: planes must be float32 or float64");
-  if (n < 0) return fail(TF_EINVAL, "tf_reduce_host: negative length");
-  if (!out) return fail(TF_EINVAL, "tf_reduce_host: null output");
+    return fail(TF_EINVAL, w + ": planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, w + ": negative length");
+  if (!out || !rops || !a) return fail(TF_EINVAL, w + ": null argument");
+  for (int r = 0; r < nred; r++)
+    if (rops[r] < 0 || rops[r] >= TF_NUM_ROPS) return fail(TF_EINVAL, w + ": unknown reduction id");
   const size_t tsz = dtype == TF_F64 ? 8 : 4;
   if (n == 0) {
-    std::memset(out, 0, 2 * tsz);
+    std::memset(out, 0, 2 * tsz * nred);
     return TF_OK;
   }
-  if (!a || (rop != TF_RSUM && !b)) return fail(TF_EINVAL, "tf_reduce_host: null plane");
-  const int npl = rop == TF_RSUM ? 1 : 2;
-  const void* src[2] = {a, rop == TF_RSUM ? a : b};
+  // distinct planes; per reduction the index of each operand among them
+  std::vector<const void*> uniq;
+  std::vector<int> ia(nred), ib(nred, -1);
+  auto intern = [&](const void* ptr) {
+    for (size_t q = 0; q < uniq.size(); q++)
+      if (uniq[q] == ptr) return (int)q;
+    uniq.push_back(ptr);
+    return (int)uniq.size() - 1;
+  };
+  for (int r = 0; r < nred; r++) {
+    if (!a[r] || (rops[r] != TF_RSUM && (!b || !b[r]))) return fail(TF_EINVAL, w + ": null plane");
+    ia[r] = intern(a[r]);
+    if (rops[r] != TF_RSUM) ib[r] = intern(b[r]);
+  }
+  const int U = (int)uniq.size();
+
   DeviceGuard g(device);
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64) return fail(TF_EINVAL, "tf_reduce_host: device ordinal");
+  if (dev < 0 || dev >= 64) return fail(TF_EINVAL, w + ": device ordinal");
   HostPipe& p = g_pipe[dev];
   RedStage& R = g_red[dev];
   std::lock_guard<std::mutex> lock(p.mu);
@@ -422,83 +453,82 @@ extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, cons
   const int64_t nchunks = (n + chunk - 1) / chunk;
   const int64_t pbytes = chunk * (int64_t)tsz;
 
-  bool pin[2] = {is_pinned(src[0]), is_pinned(src[1])};
-  const bool pageable = !pin[0] || (npl == 2 && !pin[1]);
-  if (R.plane_bytes < pbytes || !R.ws[0]) {
-    for (int s = 0; s < HostPipe::MAX_SLOTS; s++) {
-      for (int k = 0; k < 2; k++) {
-        if (R.d[s][k]) cudaFree(R.d[s][k]);
-        if (R.h[s][k]) cudaFreeHost(R.h[s][k]);
-        R.d[s][k] = R.h[s][k] = nullptr;
+  std::vector<char> pin(U);
+  bool pageable = false;
+  for (int q = 0; q < U; q++) pageable |= !(pin[q] = is_pinned(uniq[q]));
+  const size_t need_ws = reduce_ws_bytes(dtype, chunk);  // f64 needs twice f32's
+  if (R.plane_bytes < pbytes || R.ws_bytes < need_ws) {
+    red_free(R);  // set up again below; a failed setup leaves it empty and retries
+    for (int s = 0; s < p.slots; s++) {
+      cudaError_t e = cudaMalloc(&R.ws[s], need_ws);
+      if (e == cudaSuccess) e = cudaMemset(R.ws[s], 0, need_ws);
+      if (e != cudaSuccess) {
+        red_free(R);
+        return cuda_status(e, who);
       }
-      if (R.ws[s]) cudaFree(R.ws[s]);
-      R.ws[s] = nullptr;
     }
     R.plane_bytes = pbytes;
-    R.ws_bytes = reduce_ws_bytes(dtype, chunk);
-    for (int s = 0; s < p.slots; s++) {
-      for (int k = 0; k < 2; k++) {
-        cudaError_t e = cudaMalloc(&R.d[s][k], pbytes);
-        if (e != cudaSuccess) return cuda_status(e, who);
-      }
-      cudaError_t e = cudaMalloc(&R.ws[s], R.ws_bytes);
-      if (e == cudaSuccess) e = cudaMemset(R.ws[s], 0, R.ws_bytes);
+    R.ws_bytes = need_ws;
+  }
+  for (int s = 0; s < p.slots; s++) {
+    while ((int)R.d[s].size() < U) {
+      void* d = nullptr;
+      cudaError_t e = cudaMalloc(&d, R.plane_bytes);
       if (e != cudaSuccess) return cuda_status(e, who);
+      R.d[s].push_back(d);
+    }
+    while (pageable && (int)R.h[s].size() < U) {
+      void* h = nullptr;
+      cudaError_t e = cudaHostAlloc(&h, R.plane_bytes, cudaHostAllocPortable);
+      if (e != cudaSuccess) return cuda_status(e, who);
+      R.h[s].push_back(h);
     }
   }
-  if (pageable) {
-    for (int s = 0; s < p.slots; s++)
-      for (int k = 0; k < 2; k++)
-        if (!R.h[s][k]) {
-          cudaError_t e = cudaHostAlloc(&R.h[s][k], pbytes, cudaHostAllocPortable);
-          if (e != cudaSuccess) return cuda_status(e, who);
-        }
-    if ((rc = ensure_planes(p, 0, true))) return rc;  // the copy pool
-  }
-  void* parts = nullptr;  // nchunks x 2 of dtype, then the result pair
-  cudaError_t e = cudaMalloc(&parts, (size_t)(nchunks + 1) * 2 * tsz);
+  if (pageable && (rc = ensure_planes(p, 0, true))) return rc;  // the copy pool
+
+  void* parts = nullptr;  // nred x nchunks x 2 of dtype, then nred result pairs
+  cudaError_t e = cudaMalloc(&parts, (size_t)nred * (nchunks + 1) * 2 * tsz);
   if (e != cudaSuccess) return cuda_status(e, who);
+  auto part_at = [&](int r, int64_t c) {
+    return static_cast<char*>(parts) + ((size_t)r * nchunks + (size_t)c) * 2 * tsz;
+  };
+  char* res = static_cast<char*>(parts) + (size_t)nred * nchunks * 2 * tsz;
   std::vector<int64_t> counts(nchunks);
   const int S = p.slots;
   std::vector<char> busy(S, 0);
-  for (int64_t c = 0; c < nchunks; c++) {
+  for (int64_t c = 0; c < nchunks && !rc; c++) {
     const int s = (int)(c % S);
     if (busy[s]) {  // the slot's previous chunk must be done before its buffers are reused
       e = cudaEventSynchronize(p.done[s]);
-      if (e != cudaSuccess) { cudaFree(parts); return cuda_status(e, who); }
+      if (e != cudaSuccess) { rc = cuda_status(e, who); break; }
     }
     const int64_t off = c * chunk;
     const int64_t m = (n - off) < chunk ? (n - off) : chunk;
     counts[c] = m;
     const size_t bytes = (size_t)m * tsz;
     cudaStream_t st = p.st[s];
-    const void* din[2] = {nullptr, nullptr};
-    for (int k = 0; k < npl; k++) {
-      const void* from = static_cast<const char*>(src[k]) + off * tsz;
-      if (!pin[k]) {
-        par_memcpy(*p.pool, R.h[s][k], from, bytes);
-        from = R.h[s][k];
+    for (int q = 0; q < U && !rc; q++) {
+      const void* from = static_cast<const char*>(uniq[q]) + off * tsz;
+      if (!pin[q]) {
+        par_memcpy(*p.pool, R.h[s][q], from, bytes);
+        from = R.h[s][q];
       }
-      e = cudaMemcpyAsync(R.d[s][k], from, bytes, cudaMemcpyHostToDevice, st);
-      if (e != cudaSuccess) { cudaFree(parts); return cuda_status(e, who); }
-      din[k] = R.d[s][k];
+      e = cudaMemcpyAsync(R.d[s][q], from, bytes, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) rc = cuda_status(e, who);
     }
-    rc = reduce_launch(rop, dtype, m, din[0], npl == 2 ? din[1] : nullptr,
-                       static_cast<char*>(parts) + (size_t)c * 2 * tsz, R.ws[s], R.ws_bytes, st);
-    if (rc) { cudaFree(parts); return rc; }
-    e = cudaEventRecord(p.done[s], st);
-    if (e != cudaSuccess) { cudaFree(parts); return cuda_status(e, who); }
+    for (int r = 0; r < nred && !rc; r++)
+      rc = reduce_launch(rops[r], dtype, m, R.d[s][ia[r]], ib[r] >= 0 ? R.d[s][ib[r]] : nullptr,
+                         part_at(r, c), R.ws[s], R.ws_bytes, st);
+    if (!rc && (e = cudaEventRecord(p.done[s], st)) != cudaSuccess) rc = cuda_status(e, who);
     busy[s] = 1;
   }
-  for (int s = 0; s < S; s++)
-    if (busy[s] && (e = cudaEventSynchronize(p.done[s])) != cudaSuccess) {
-      cudaFree(parts);
-      return cuda_status(e, who);
-    }
-  void* res = static_cast<char*>(parts) + (size_t)nchunks * 2 * tsz;
-  rc = combine_launch(dtype, (int)nchunks, parts, counts.data(), res, p.st[0]);
+  for (int s = 0; s < S && !rc; s++)
+    if (busy[s] && (e = cudaEventSynchronize(p.done[s])) != cudaSuccess) rc = cuda_status(e, who);
+  for (int r = 0; r < nred && !rc; r++)
+    rc = combine_launch(dtype, (int)nchunks, part_at(r, 0), counts.data(), res + (size_t)r * 2 * tsz,
+                        p.st[0]);
   if (!rc) {
-    e = cudaMemcpyAsync(out, res, 2 * tsz, cudaMemcpyDeviceToHost, p.st[0]);
+    e = cudaMemcpyAsync(out, res, (size_t)nred * 2 * tsz, cudaMemcpyDeviceToHost, p.st[0]);
     if (e == cudaSuccess) e = cudaStreamSynchronize(p.st[0]);
     if (e != cudaSuccess) rc = cuda_status(e, who);
   }
@@ -507,6 +537,19 @@ extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, cons
     for (int s = 0; s < p.slots; s++) cudaStreamSynchronize(p.st[s]);
   cudaFree(parts);
   return rc;
+}
+}  // namespace tf
+
+extern "C" int tf_reduce_host(int rop, int dtype, int64_t n, const void* a, const void* b,
+                              void* out, int device) {
+  const void* bb[1] = {b};
+  return reduce_host_batch(1, &rop, dtype, n, &a, bb, out, device, "tf_reduce_host");
+}
+
+extern "C" int tf_reduce_host_batch(int nred, const int* rops, int dtype, int64_t n,
+                                    const void* const* a, const void* const* b, void* out,
+                                    int device) {
+  return reduce_host_batch(nred, rops, dtype, n, a, b, out, device, "tf_reduce_host_batch");
 }
 
 // ---- page-locking of reused pageable planes ------------------------------------
@@ -526,6 +569,13 @@ extern "C" int tf_host_register(void* ptr, size_t bytes) {
 
 extern "C" int tf_host_unregister(void* ptr) {
   if (!ptr) return fail(TF_EINVAL, "tf_host_unregister: null pointer");
+  // A host call on another thread may be DMA-ing this plane in place (it was
+  // pinned when that call checked).  Host calls hold their device's pipe lock
+  // for their whole duration, so taking every pipe lock (in index order; a call
+  // holds only one) waits for them; later calls see the plane as pageable.
+  std::vector<std::unique_lock<std::mutex>> held;
+  held.reserve(64);
+  for (auto& pp : g_pipe) held.emplace_back(pp.mu);
   cudaError_t e = cudaHostUnregister(ptr);
   if (e != cudaSuccess) {
     cudaGetLastError();

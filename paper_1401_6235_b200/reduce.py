@@ -132,6 +132,58 @@ def vtdot(x, y, out=None):
     return _reduce("vtdot", "dot", (x, y), out)
 
 
+def host_batch(calls, device=None):
+    """Several reductions over host (numpy) planes in ONE pipelined pass.
+
+    ``calls`` is a list of ``("vtsum", x)``, ``("vtsum2", (x0, x1))`` or
+    ``("vtdot", x, y)``; all planes share one length and dtype.  Each distinct
+    plane crosses the host link once however many reductions read it, so
+    ``[("vtdot", x, y), ("vtsum", x)]`` moves x once.  Returns one ``Twofold`` per
+    call, bit-identical to the calls made one by one (tf_reduce_host_batch).
+    """
+    if not calls:
+        return []
+    rops, a_ptrs, b_ptrs, first, seen = [], [], [], None, []
+    for call in calls:
+        name = call[0]
+        if name == "vtsum":
+            rop, ins = "sum", (call[1],)
+        elif name == "vtsum2":
+            rop, ins = "sum2", tuple(call[1])
+        elif name == "vtdot":
+            rop, ins = "dot", (call[1], call[2])
+        else:
+            raise ValueError("host_batch: unknown reduction %r" % (name,))
+        planes = [_describe(name, p) for p in ins]
+        seen.extend(planes)
+        for p in planes:
+            if p.kind != "host":
+                raise ValueError("%s: host_batch takes numpy (host) planes" % name)
+            if first is None:
+                first = p
+            elif p.dtype != first.dtype:
+                raise ValueError("%s: planes mix %s and %s" % (name, first.dtype, p.dtype))
+            elif p.n != first.n:
+                raise ValueError("%s: plane lengths differ (%d vs %d)" % (name, first.n, p.n))
+        rops.append(_lib.ROP_IDS[rop])
+        a_ptrs.append(planes[0].ptr)
+        b_ptrs.append(planes[1].ptr if len(planes) > 1 else None)
+    from .kernels import _maybe_register
+
+    for p in seen:
+        if isinstance(p.obj, np.ndarray):
+            _maybe_register(p.obj)
+    dev = device if device is not None else (torch.cuda.current_device() if torch is not None else 0)
+    _lib.ensure_device(dev)
+    res = np.zeros((len(calls), 2), first.dtype)
+    arr = (ctypes.c_int * len(rops))(*rops)
+    rc = _lib.lib().tf_reduce_host_batch(len(rops), arr, _dtype_id(first.dtype), first.n,
+                                         _lib.ptr_array(a_ptrs), _lib.ptr_array(b_ptrs),
+                                         res.ctypes.data, dev)
+    _lib.check(rc, "host_batch")
+    return [Twofold(float(r[0]), float(r[1])) for r in res]
+
+
 def combine(partials, counts, out=None):
     """Adjacent-pair ``_tadd`` tree over per-shard partials (g x 2 CUDA tensor)."""
     p = partials.contiguous()
@@ -183,5 +235,5 @@ def binomial_coeffs(degree=20):
     return [float((-1) ** (degree - k) * comb(degree, k)) for k in range(degree + 1)]
 
 
-__all__ = ["Twofold", "vtsum", "vtsum2", "vtdot", "vthorner", "combine", "geometry",
+__all__ = ["Twofold", "vtsum", "vtsum2", "vtdot", "vthorner", "combine", "host_batch", "geometry",
            "tile_elems", "binomial_coeffs", "TwofoldArray"]

@@ -258,6 +258,68 @@ def test_host_plane_reductions_match_device(oracle, rop, pin, dtype):
     assert (zh.value, zh.error) == (zd.value, zd.error) == (float(w[0]), float(w[1]))
 
 
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("pin", [False, True])
+def test_host_reduction_batch_matches_single_calls(oracle, pin, dtype):
+    # several reductions in one pass over shared host planes (x crosses once):
+    # every result equals the single call and the oracle, in call order
+    from paper_1401_6235_b200 import reduce as R
+
+    rng = np.random.default_rng(31)
+    n = 21 * 131072 + 999
+    tdt = torch.float64 if dtype == np.float64 else torch.float32
+
+    def plane(a):
+        a = a.astype(dtype)
+        if not pin:
+            return a
+        p = torch.empty(n, dtype=tdt, pin_memory=True).numpy()
+        p[:] = a
+        return p
+
+    x = plane(rng.uniform(-1, 1, n) * np.exp2(rng.integers(-25, 26, n)))
+    y = plane(rng.uniform(-1, 1, n))
+    e = plane(x * 2.0**-40 * rng.uniform(-1, 1, n))
+    calls = [("vtdot", x, y), ("vtsum", x), ("vtsum2", (x, e)), ("vtdot", y, y), ("vtsum", y)]
+    got = R.host_batch(calls)
+    g = _geom(dtype)
+    want = [oracle.reduce("dot", x, y, geometry=g), oracle.reduce("sum", x, geometry=g),
+            oracle.reduce("sum2", x, e, geometry=g), oracle.reduce("dot", y, y, geometry=g),
+            oracle.reduce("sum", y, geometry=g)]
+    single = [R.vtdot(x, y), R.vtsum(x), R.vtsum2((x, e)), R.vtdot(y, y), R.vtsum(y)]
+    for z, w, s1 in zip(got, want, single):
+        assert (z.value, z.error) == (float(w[0]), float(w[1])) == (s1.value, s1.error)
+    assert R.host_batch([]) == []
+    with pytest.raises(ValueError, match="plane lengths differ"):
+        R.host_batch([("vtsum", x), ("vtsum", y[:-1])])
+    with pytest.raises(ValueError, match="unknown reduction"):
+        R.host_batch([("vtmax", x)])
+    z0 = R.host_batch([("vtsum", x[:0]), ("vtdot", x[:0], y[:0])])
+    assert all(np.copysign(1, v.value) == 1 and v.value == 0 and v.error == 0 for v in z0)
+
+
+def test_host_plane_reduction_f32_then_f64_fresh_process():
+    # the host-reduction staging is sized by the first call; an f64 call after an
+    # f32 one (same chunk bytes, twice the tile-partial bytes) must regrow it
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, torch\n"
+        "from paper_1401_6235_b200 import reduce as R\n"
+        "rng = np.random.default_rng(5)\n"
+        "n = 9 * 131072 + 3\n"
+        "x32 = rng.uniform(-1, 1, n).astype(np.float32)\n"
+        "x64 = rng.uniform(-1, 1, n)\n"
+        "for x in (x32, x64, x32):\n"
+        "    zh = R.vtsum(x); zd = R.vtsum(torch.as_tensor(x, device='cuda'))\n"
+        "    assert (zh.value, zh.error) == (zd.value, zd.error), (zh, zd)\n"
+        "print('ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=str(GOLDEN.parents[1]))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
 def test_horner_host_planes_match_device(oracle):
     from paper_1401_6235_b200 import kernels as K
     from paper_1401_6235_b200 import reduce as R
