@@ -50,7 +50,7 @@ __device__ __forceinline__ void scalar_elem(const Planes<T>& p, int64_t i) {
 
 template <class T, int OP, int VB>
 __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t head,
-                                                 int64_t nvec) {
+                                                 int64_t nvec, int reps) {
   constexpr int NIN = OpInfo<OP>::NIN;
   using V = VecN<T, VB>;
   constexpr int E = V::N;
@@ -71,15 +71,15 @@ __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t
   V* vo0 = reinterpret_cast<V*>(p.out[0] + head);
   V* vo1 = reinterpret_cast<V*>(p.out[1] + head);
 
-  // CTA-chunked: chunk c = vectors [c*CH, (c+1)*CH), CH = 256*U*R; thread t
+  // CTA-chunked: chunk c = vectors [c*CH, (c+1)*CH), CH = 256*U*reps; thread t
   // takes t, t+256, ... (coalesced).  With one CTA per chunk the hardware block
   // scheduler balances SMs dynamically (no tail of idle SMs); a capped grid
-  // strides over chunks.
-  constexpr int R = 4;
-  constexpr int64_t CH = 256LL * U * R;
+  // strides over chunks.  reps = 4 on large planes; small planes use shorter
+  // chunks so that the grid still covers every SM evenly.
+  const int64_t CH = 256LL * U * reps;
   for (int64_t cb = (int64_t)blockIdx.x * CH; cb < nvec; cb += (int64_t)gridDim.x * CH) {
 #pragma unroll 1
-    for (int rr = 0; rr < R; rr++) {
+    for (int rr = 0; rr < reps; rr++) {
       const int64_t base = cb + (int64_t)rr * 256 * U + threadIdx.x;
       V r[U][NIN];
 #pragma unroll
@@ -199,11 +199,15 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     mbs = b > 0 ? b : 1;
     ent.max_blocks_per_sm.store(mbs, std::memory_order_relaxed);
   }
-  // one CTA per chunk of 256*U*4 vectors (hardware-balanced); TF_EW_SCHED=
-  // persistent caps the grid at the resident CTAs instead (A/B measurements)
-  const int64_t chunk = 256LL * ent.unroll * 4;
-  int64_t blocks = nvec > 0 ? (nvec + chunk - 1) / chunk : (n + 255) / 256;
+  // one CTA per chunk of 256*U*reps vectors (hardware-balanced); reps = 4
+  // unless that leaves fewer than two full waves of resident CTAs (small
+  // planes, e.g. 2^20 elements: 256 CTAs of 4 steps ran 1.7 uneven waves).
+  // TF_EW_SCHED=persistent caps the grid at the resident CTAs (A/B runs).
   const int64_t resident = (int64_t)sm_count() * mbs;
+  int reps = 4;
+  while (reps > 1 && nvec / (256LL * ent.unroll * reps) < 2 * resident) reps >>= 1;
+  const int64_t chunk = 256LL * ent.unroll * reps;
+  int64_t blocks = nvec > 0 ? (nvec + chunk - 1) / chunk : (n + 255) / 256;
   static const bool persistent = [] {
     const char* e = getenv("TF_EW_SCHED");
     return e && e[0] == 'p';
@@ -216,7 +220,7 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
   for (int k = 0; k < ent.nin; k++) p.in[k] = static_cast<const double*>(in[k]);
   p.out[0] = static_cast<double*>(out[0]);
   p.out[1] = static_cast<double*>(out[1]);
-  void* args[] = {&p, &n, &head, &nvec};
+  void* args[] = {&p, &n, &head, &nvec, &reps};
   cudaError_t e = cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, stream);
   return cuda_status(e, "tf_elementwise: launch");
 }
