@@ -293,7 +293,8 @@ def max_over_ranks(x, world):
     return float(t.item())
 
 
-def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3, planes_of=None):
+def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3, planes_of=None,
+                             nthreads=None):
     """Oracle port (plain C, OpenMP, all host threads) on a bounded sample.
     planes_of(name) returns the op's host input planes (the first n_sample
     elements of the bench's own device planes); else dists_host generates them."""
@@ -303,7 +304,7 @@ def cpu_baseline_elementwise(ops_names, dists_host, dtype, n_sample, reps=3, pla
     planes = {}
     total_units = 0
     t_total = 0.0
-    nt = os.cpu_count() or 1
+    nt = nthreads or os.cpu_count() or 1
     out = (np.zeros(n_sample, dtype), np.zeros(n_sample, dtype))
     for name in ops_names:
         ins = planes_of(name) if planes_of else dists_host(name, rng, n_sample)
@@ -687,10 +688,14 @@ def run_elementwise(args, rank, world, local):
             return [p[:ns].cpu().numpy() for p in ps.planes(name)]
 
         v, nt, per = cpu_baseline_elementwise(wl["names"], gen, dtype, ns, planes_of=planes_of)
+        ns1 = min(ns, 1 << 23)  # one core: a smaller sample of the same planes
+        v1, _, _ = cpu_baseline_elementwise(wl["names"], gen, dtype, ns1, nthreads=1,
+                                            planes_of=lambda name: [p[:ns1] for p in planes_of(name)])
         cpu = {"value": v, "unit": "elem-ops/s", "cores": nt, "kind": "port",
                "sample": "first %d elements of the bench's own input planes per op over %s "
                          "(best of 3 per op), oracle/twofold_oracle.c OpenMP on %d threads"
-                         % (ns, "/".join(wl["names"]), nt)}
+                         % (ns, "/".join(wl["names"]), nt),
+               "single_core": {"value": v1, "cores": 1, "sample": "first %d elements per op" % ns1}}
 
     log("done")
     if rank == 0:
