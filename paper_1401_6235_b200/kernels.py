@@ -174,6 +174,11 @@ def _check(name, ins, outs):
         raise ValueError("%s: planes live on different devices" % name)
     pin, pout = planes[: len(ins)], planes[len(ins):]
     for o in pout:
+        # the reference's numba loop refuses a read-only out array at call time;
+        # here the library would write through the pointer, so refuse up front
+        if isinstance(o.obj, np.ndarray) and not o.obj.flags.writeable:
+            raise ValueError("%s: out planes must be writeable" % name)
+    for o in pout:
         for a in pin:
             if _overlap(o, a):
                 raise ValueError("%s: out must not alias an input" % name)

@@ -132,6 +132,20 @@ def test_rejections_happen_before_any_launch():
         K.vtadd2(x, y, K.TwofoldArray(same, same))
 
 
+def test_read_only_out_is_rejected():
+    # a read-only numpy out plane (np.frombuffer over bytes, a read-only mmap)
+    # is refused before anything is written through its pointer
+    from paper_1401_6235_b200 import kernels as K
+
+    x, y, out = _fresh()
+    ro = np.frombuffer(bytes(8 * 8), dtype=np.float64)
+    with pytest.raises(ValueError, match="writeable"):
+        K.vtadd2(x, y, K.TwofoldArray(ro, out.error))
+    assert np.all(ro == 0) and np.all(out.error == 7.0)
+    # read-only INPUTS are fine (the reference reads them too)
+    assert not ro.flags.writeable
+
+
 def test_partial_overlap_is_aliasing():
     from paper_1401_6235_b200 import kernels as K
 
