@@ -184,6 +184,10 @@ extern "C" int tf_xgpu_open(int device, int world, int rank, const void* handles
     return fail(TF_EINVAL, "tf_xgpu_open: bad arguments");
   std::lock_guard<std::mutex> lock(c->mu);
   if (!c->own) return fail(TF_EINVAL, "tf_xgpu_open: call tf_xgpu_mailbox first");
+  // A second transport in the same job (same group): the peers' mailboxes are
+  // process-lifetime allocations, already mapped — reuse them.
+  if (c->world == world && c->rank == rank) return TF_OK;
+  if (c->world > 1) return fail(TF_EINVAL, "tf_xgpu_open: already open for another group");
   for (int r = 0; r < world; r++) {
     if (r == rank) {
       c->box[r] = c->own;
