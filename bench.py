@@ -60,8 +60,9 @@ def parse():
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay each step as a CUDA graph (auto: n <= 2^22, launch-bound)")
     ap.add_argument("--reduce-transport", choices=["nccl", "p2p"], default="nccl",
-                    help="config4 cross-GPU combine: NCCL all-gather + tf_combine, or the "
-                         "NVLink peer-memory mailboxes (csrc/xgpu.cu)")
+                    help="config4 cross-GPU combine: NCCL all-gather + tf_combine, or each "
+                         "reduction fused with the NVLink peer-memory exchange in one launch "
+                         "(tf_xgpu_reduce, csrc/xgpu.cu)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26,
@@ -751,18 +752,27 @@ def run_config4(args, rank, world, local):
     tp = D.P2PTransport() if args.reduce_transport == "p2p" else None
 
     def cross(p):  # the one exchange step: partials of every rank -> global twofold
-        if world == 1:
-            return
-        if tp is not None:
-            tp.combine(p, counts)  # NVLink mailboxes, no NCCL
-        else:
+        if world > 1:
             R.combine(D.gather_partials(p), counts, out=p)  # NCCL all-gather + tf_combine
 
+    def dot():
+        if tp is not None:  # reduction + NVLink exchange fused in one launch, no NCCL
+            tp.reduce("dot", (X, Y), counts, out=part)
+        else:
+            R.vtdot(X, Y, out=part)
+
+    def vsum():
+        if tp is not None:
+            tp.reduce("sum", (X,), counts, out=part2)
+        else:
+            R.vtsum(X, out=part2)
+            cross(part2)
+
     def step():
-        R.vtdot(X, Y, out=part)
-        cross(part)
-        R.vtsum(X, out=part2)
-        cross(part2)
+        dot()
+        if tp is None:
+            cross(part)
+        vsum()
 
     for _ in range(args.warmup):
         step()
@@ -777,11 +787,11 @@ def run_config4(args, rank, world, local):
         start.record(stream)
         for s in range(K):
             ev[s][0].record(stream)
-            R.vtdot(X, Y, out=part)
+            dot()
             ev[s][1].record(stream)
-            cross(part)
-            R.vtsum(X, out=part2)
-            cross(part2)
+            if tp is None:
+                cross(part)
+            vsum()
         end.record(stream)
         torch.cuda.synchronize()
     barrier(world)
@@ -835,7 +845,7 @@ def run_config4(args, rank, world, local):
                                         "x crosses the link once (tf_reduce_host_batch)",
                                 "h2d_bytes_per_step": 16 * n}},
             "cpu_baseline": cpu,
-            "gpu_launches": world * K * (2 + (2 if world > 1 else 0)),
+            "gpu_launches": world * K * (2 + (2 if world > 1 and tp is None else 0)),
             "reduce_transport": args.reduce_transport if world > 1 else "none (1 GPU)",
             "clocks": clk.summary(),
         }

@@ -24,95 +24,30 @@
 #include <string>
 
 #include "common.cuh"
+#include "reduce_impl.cuh"
 #include "tf_math.cuh"
+#include "xgpu.cuh"
 
 namespace tf {
-
-constexpr int XG_MAXG = 64;
-
-struct Slot {
-  double z0, z1;
-  unsigned long long seq;
-  unsigned long long pad;
-};
-
-struct XArgs {
-  Slot* box[XG_MAXG];  // mailbox base of every rank, as mapped on this device
-  int rank, world;
-  unsigned long long epoch;
-  unsigned long long nonempty_lo, nonempty_hi;  // bitmask of ranks with count > 0
-};
-
-template <class T>
-__device__ __forceinline__ P<T> xcomb(P<T> l, P<T> r) {
-  return tadd(l.a, l.b, r.a, r.b);
-}
-
-// The protocol, for one rank; run by one thread.  Shared by the real transport
-// kernel (one rank per GPU) and the one-GPU emulation (one rank per block).
-template <class T>
-__device__ void xgpu_exchange(T* out, const XArgs& x, int* status) {
-  const int par = (int)(x.epoch & 1);
-  const volatile T* mine_v = out;
-  const double z0 = (double)mine_v[0], z1 = (double)mine_v[1];
-  // 1. publish: data everywhere, one system fence, then the flags
-  for (int r = 0; r < x.world; r++) {
-    volatile Slot* s = x.box[r] + par * XG_MAXG + x.rank;
-    s->z0 = z0;
-    s->z1 = z1;
-  }
-  __threadfence_system();
-  for (int r = 0; r < x.world; r++) {
-    volatile Slot* s = x.box[r] + par * XG_MAXG + x.rank;
-    s->seq = x.epoch;
-  }
-  // 2. wait for every rank's slot of this epoch in the local mailbox
-  volatile Slot* mine = x.box[x.rank] + par * XG_MAXG;
-  const long long t0 = clock64();
-  for (int r = 0; r < x.world; r++) {
-    while (mine[r].seq != x.epoch) {
-      if (clock64() - t0 > 20000000000LL) {  // ~10 s at 2 GHz: give up, never hang
-        out[0] = out[1] = T(NAN);
-        *status = 1;
-        return;
-      }
-    }
-  }
-  __threadfence_system();
-  // 3. skip tree over the non-empty ranks, in rank order (as tf_combine)
-  P<T> st[8];
-  int lv[8];
-  int sp = 0, m = 0;
-  for (int r = 0; r < x.world; r++) {
-    const bool present = r < 64 && ((r < 32 ? (x.nonempty_lo >> r) : (x.nonempty_hi >> (r - 32))) & 1ull);
-    if (!present) continue;
-    P<T> v{(T)mine[r].z0, (T)mine[r].z1};
-    m++;
-    int l = 0;
-    while (sp > 0 && lv[sp - 1] == l) {
-      v = xcomb(st[sp - 1], v);
-      sp--;
-      l++;
-    }
-    st[sp] = v;
-    lv[sp] = l;
-    sp++;
-  }
-  if (m == 0) {
-    out[0] = T(0);
-    out[1] = T(0);
-    return;
-  }
-  P<T> acc = st[sp - 1];
-  for (int s = sp - 2; s >= 0; s--) acc = xcomb(st[s], acc);
-  out[0] = acc.a;
-  out[1] = acc.b;
-}
 
 template <class T>
 __global__ void xgpu_exchange_kernel(T* out, XArgs x, int* status) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   xgpu_exchange(out, x, status);
+}
+
+// Reduction fused with the exchange: every CTA reduces its tile as in
+// reduce_kernel; the last CTA, having folded the tile tree into out[0..1], runs
+// the mailbox protocol from the same thread — the local result goes straight to
+// the peers over NVLink and the global result lands in out, in ONE launch.
+template <class T, int ROP, bool VEC>
+__global__ void __launch_bounds__(RW) reduce_xgpu_kernel(const T* __restrict__ a,
+                                                         const T* __restrict__ b, int64_t n,
+                                                         int64_t ntiles, P<T>* tiles,
+                                                         unsigned* counter, T* out, XArgs x,
+                                                         int* status) {
+  if (reduce_tile<T, ROP, VEC>(a, b, n, ntiles, tiles, counter, out) && threadIdx.x == 0)
+    xgpu_exchange(out, x, status);
 }
 
 // One-GPU emulation of `world` ranks: block r plays rank r over mailboxes that
@@ -143,6 +78,21 @@ struct XCtx {
   int* status = nullptr;
 };
 static XCtx g_x[64];
+
+// Arguments of this rank's next exchange (caller holds c.mu): one epoch per call.
+static XArgs next_exchange(XCtx& c, const int64_t* counts) {
+  XArgs x{};
+  for (int r = 0; r < c.world; r++) x.box[r] = c.box[r];
+  x.rank = c.rank;
+  x.world = c.world;
+  x.epoch = ++c.epoch;
+  for (int r = 0; r < c.world; r++)
+    if (counts[r] > 0) {
+      if (r < 32) x.nonempty_lo |= 1ull << r;
+      else x.nonempty_hi |= 1ull << (r - 32);
+    }
+  return x;
+}
 
 static XCtx* ctx_for_current(int* dev_out) {
   int dev = 0;
@@ -213,22 +163,76 @@ extern "C" int tf_xgpu_combine(int dtype, void* out, const int64_t* counts, void
   if ((dtype != TF_F32 && dtype != TF_F64) || !out || !counts)
     return fail(TF_EINVAL, "tf_xgpu_combine: bad arguments");
   std::lock_guard<std::mutex> lock(c->mu);
-  XArgs x{};
-  for (int r = 0; r < c->world; r++) x.box[r] = c->box[r];
-  x.rank = c->rank;
-  x.world = c->world;
-  x.epoch = ++c->epoch;
-  for (int r = 0; r < c->world; r++)
-    if (counts[r] > 0) {
-      if (r < 32) x.nonempty_lo |= 1ull << r;
-      else x.nonempty_hi |= 1ull << (r - 32);
-    }
+  XArgs x = next_exchange(*c, counts);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dtype == TF_F64)
     xgpu_exchange_kernel<double><<<1, 32, 0, s>>>(static_cast<double*>(out), x, c->status);
   else
     xgpu_exchange_kernel<float><<<1, 32, 0, s>>>(static_cast<float*>(out), x, c->status);
   return launch_status("tf_xgpu_combine");
+}
+
+namespace tf {
+size_t reduce_ws_bytes(int dtype, int64_t n);
+
+template <class T, int ROP>
+static void launch_reduce_xgpu(int64_t n, const void* a, const void* b, void* out, void* ws,
+                               const XArgs& x, int* status, cudaStream_t s) {
+  const int64_t nt = (n + Geo<T>::L - 1) / Geo<T>::L;
+  unsigned* counter = static_cast<unsigned*>(ws);
+  P<T>* tiles = reinterpret_cast<P<T>*>(static_cast<char*>(ws) + 256);
+  const T* pa = static_cast<const T*>(a);
+  const T* pb = static_cast<const T*>(b ? b : a);
+  T* po = static_cast<T*>(out);
+  if (aligned16(a) && (ROP == TF_RSUM || aligned16(b)))
+    reduce_xgpu_kernel<T, ROP, true><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
+                                                                 po, x, status);
+  else
+    reduce_xgpu_kernel<T, ROP, false><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
+                                                                  po, x, status);
+}
+}  // namespace tf
+
+// Reduce this rank's shard AND exchange/combine over NVLink in one launch:
+// tf_reduce followed by tf_xgpu_combine, fused (the last CTA publishes the local
+// result to the peers' mailboxes, waits for theirs and folds them).  Same
+// arguments as tf_reduce plus the host array of world shard sizes; out holds the
+// global result on completion.  Collective, like tf_xgpu_combine.
+extern "C" int tf_xgpu_reduce(int rop, int dtype, int64_t n, const void* a, const void* b,
+                              void* out, void* ws, size_t ws_bytes, const int64_t* counts,
+                              void* stream) {
+  XCtx* c = ctx_for_current(nullptr);
+  if (!c || c->world < 1) return fail(TF_EINVAL, "tf_xgpu_reduce: transport not open");
+  if (rop < 0 || rop >= TF_NUM_ROPS) return fail(TF_EINVAL, "tf_xgpu_reduce: unknown reduction id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, "tf_xgpu_reduce: planes must be float32 or float64");
+  if (n < 0 || !out || !counts) return fail(TF_EINVAL, "tf_xgpu_reduce: bad arguments");
+  if (n > 0 && (!a || (rop != TF_RSUM && !b))) return fail(TF_EINVAL, "tf_xgpu_reduce: null plane");
+  if (n > 0 && (!ws || ws_bytes < reduce_ws_bytes(dtype, n)))
+    return fail(TF_EINVAL, "tf_xgpu_reduce: workspace too small");
+  const int64_t L = dtype == TF_F64 ? Geo<double>::L : Geo<float>::L;
+  if ((n + L - 1) / L > 0x7fffffffLL) return fail(TF_EINVAL, "tf_xgpu_reduce: too many tiles");
+  std::lock_guard<std::mutex> lock(c->mu);
+  XArgs x = next_exchange(*c, counts);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  if (n == 0) {  // nothing to reduce: (+0, +0), skipped by the fold (count 0)
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * tsz, s);
+    if (e != cudaSuccess) return cuda_status(e, "tf_xgpu_reduce");
+    if (dtype == TF_F64)
+      xgpu_exchange_kernel<double><<<1, 32, 0, s>>>(static_cast<double*>(out), x, c->status);
+    else
+      xgpu_exchange_kernel<float><<<1, 32, 0, s>>>(static_cast<float*>(out), x, c->status);
+    return launch_status("tf_xgpu_reduce");
+  }
+#define XR(ROP)                                                                            \
+  case ROP:                                                                                \
+    if (dtype == TF_F64) launch_reduce_xgpu<double, ROP>(n, a, b, out, ws, x, c->status, s); \
+    else launch_reduce_xgpu<float, ROP>(n, a, b, out, ws, x, c->status, s);                 \
+    break;
+  switch (rop) { XR(TF_RSUM) XR(TF_RSUM2) XR(TF_RDOT) }
+#undef XR
+  return launch_status("tf_xgpu_reduce");
 }
 
 // 0 = OK, 1 = a combine timed out waiting for a peer (synchronous read).

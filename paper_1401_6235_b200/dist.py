@@ -93,6 +93,11 @@ def sharded_reduce(rop: str, local: Sequence, n: int, group=None,
     if local[0].shape[0] != hi - lo:
         raise ValueError("sharded_reduce: rank %d holds %d elements, its shard is %d"
                          % (rank, local[0].shape[0], hi - lo))
+    if transport is not None and reduce_fn is None:
+        # NVLink peer-memory path: local reduction and exchange in ONE launch
+        counts = shard_counts(n, world, tile)
+        v = transport.reduce(rop, local, counts).cpu().tolist()
+        return R.Twofold(v[0], v[1])
     if reduce_fn is None:
         fn = {"sum": R.vtsum, "sum2": lambda a, b, out: R.vtsum2((a, b), out=out),
               "dot": R.vtdot}[rop]
@@ -162,6 +167,36 @@ class P2PTransport:
             rc = self._lib.lib().tf_xgpu_combine(dt, partial.data_ptr(), c, s)
         self._lib.check(rc, "P2PTransport.combine")
         return partial
+
+    def reduce(self, rop, planes, counts, out=None):
+        """This rank's reduction of ``planes`` (its shard, CUDA tensors) fused with
+        the exchange: ONE launch (tf_xgpu_reduce) leaves the global twofold in
+        ``out`` (a 2-element CUDA tensor; allocated if None) on the current stream."""
+        import ctypes
+
+        from . import reduce as R
+        from .kernels import _describe, _dtype_id
+
+        ps = [_describe("P2PTransport.reduce", p) for p in planes]
+        first = ps[0]
+        if any(p.kind != "cuda" for p in ps):
+            raise ValueError("P2PTransport.reduce: planes must be CUDA tensors")
+        if any(p.n != first.n or p.dtype != first.dtype for p in ps):
+            raise ValueError("P2PTransport.reduce: planes differ in length or dtype")
+        dt = _dtype_id(first.dtype)
+        tdt = torch.float64 if dt == self._lib.TF_F64 else torch.float32
+        if out is None:
+            out = torch.empty(2, dtype=tdt, device="cuda:%d" % first.device)
+        ws = R.workspace(first.device, dt, max(first.n, 1))
+        c = (ctypes.c_int64 * self.world)(*[int(v) for v in counts])
+        with torch.cuda.device(first.device):
+            s = torch.cuda.current_stream(first.device).cuda_stream
+            rc = self._lib.lib().tf_xgpu_reduce(
+                self._lib.ROP_IDS[rop], dt, first.n, first.ptr,
+                ps[1].ptr if len(ps) > 1 else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                c, s)
+        self._lib.check(rc, "P2PTransport.reduce")
+        return out
 
     def status(self):
         return self._lib.lib().tf_xgpu_status(self.dev)

@@ -358,6 +358,34 @@ def test_p2p_transport_single_rank_matches_combine():
     assert tp.status() == 0
 
 
+def test_p2p_fused_reduce_single_rank_matches_reduction():
+    # tf_xgpu_reduce: the reduction and the mailbox exchange in ONE launch (the
+    # last CTA publishes, waits and folds); at world 1 it must return exactly the
+    # plain reduction, for every rop, both dtypes, unaligned views and n == 0,
+    # interleaved with combine() calls (one shared epoch sequence)
+    from paper_1401_6235_b200 import dist as D
+    from paper_1401_6235_b200 import reduce as R
+
+    tp = D.P2PTransport()
+    tp2 = D.P2PTransport()  # a second transport in the same job reuses the mapping
+    rng = np.random.default_rng(77)
+    for trial, n in enumerate([5 * 65536, 3 * 131072 + 77, 1, 0, 65536 * 40 + 3]):
+        for tdt in (torch.float64, torch.float32):
+            x = _t(rng.uniform(-1, 1, n + 1) * np.exp2(rng.integers(-20, 21, n + 1))).to(tdt)
+            y = _t(rng.uniform(-1, 1, n + 1)).to(tdt)
+            for xs, ys in ((x[:n], y[:n]), (x[1:], y[1:])):  # aligned and unaligned
+                for rop, planes, ref in (("sum", (xs,), lambda: R.vtsum(xs)),
+                                         ("sum2", (xs, ys), lambda: R.vtsum2((xs, ys))),
+                                         ("dot", (xs, ys), lambda: R.vtdot(xs, ys))):
+                    want = ref()
+                    got = (tp if trial % 2 else tp2).reduce(rop, planes, [n]).cpu().tolist()
+                    assert (got[0], got[1]) == (want.value, want.error), (rop, n, tdt)
+                    part = torch.tensor([want.value, want.error], dtype=tdt, device=DEV)
+                    tp.combine(part, [n])
+                    assert part.cpu().tolist() == [want.value, want.error]
+    assert tp.status() == 0
+
+
 @pytest.mark.parametrize("world", [2, 3, 5, 8, 13, 64])
 @pytest.mark.parametrize("tdt", [torch.float64, torch.float32])
 def test_p2p_protocol_emulated_ranks_match_combine(world, tdt):
