@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(RW) reduce_kernel(const T* __restrict__ a,
                                                     const T* __restrict__ b, int64_t n,
                                                     int64_t ntiles, P<T>* tiles,
                                                     unsigned* counter, T* out) {
-  reduce_tile<T, ROP, VEC>(a, b, n, ntiles, tiles, counter, out);
+  reduce_tile<T, ROP, VEC>(a, b, n, ntiles, tiles, counter, out, blockIdx.x);
 }
 
 // ---- variant 2: TMA bulk-copy path (cp.async.bulk -> smem ring, mbarriers) ------

@@ -173,16 +173,15 @@ __device__ __forceinline__ bool finish_tile(P<T> acc, int have, int64_t t, int64
 }
 
 // ---- variant 1: register path (LDG.128 batches) --------------------------------
-// One tile per CTA; returns true in the last CTA (after it wrote out[0..1]).
+// Tile t, one per CTA; returns true in the last CTA (after it wrote out[0..1]).
 template <class T, int ROP, bool VEC>
 __device__ __forceinline__ bool reduce_tile(const T* __restrict__ a, const T* __restrict__ b,
                                             int64_t n, int64_t ntiles, P<T>* tiles,
-                                            unsigned* counter, T* out) {
+                                            unsigned* counter, T* out, int64_t t) {
   constexpr int V = Geo<T>::V;
   constexpr int64_t L = Geo<T>::L;
   using Vt = typename Vec16<T>::type;
   const int w = threadIdx.x;
-  const int64_t t = blockIdx.x;
   const int64_t base = t * L;
   P<T> acc{T(0), T(0)};
   int have = 0;

@@ -46,7 +46,46 @@ __global__ void __launch_bounds__(RW) reduce_xgpu_kernel(const T* __restrict__ a
                                                          int64_t ntiles, P<T>* tiles,
                                                          unsigned* counter, T* out, XArgs x,
                                                          int* status) {
-  if (reduce_tile<T, ROP, VEC>(a, b, n, ntiles, tiles, counter, out) && threadIdx.x == 0)
+  if (reduce_tile<T, ROP, VEC>(a, b, n, ntiles, tiles, counter, out, blockIdx.x) &&
+      threadIdx.x == 0)
+    xgpu_exchange(out, x, status);
+}
+
+// One-GPU emulation of the FUSED path for `world` ranks: one grid, tpr CTAs per
+// rank (block r*tpr + t is tile t of rank r's contiguous shard), per-rank
+// workspaces, and the mailboxes of every rank in this GPU's memory.  Each
+// rank's last CTA runs the exchange exactly as reduce_xgpu_kernel does.  At most
+// `world` CTAs ever spin, far fewer than the resident slots, so every other CTA
+// keeps making progress on one device.
+struct EmuShards {
+  int64_t lo[XG_MAXG], n[XG_MAXG];
+};
+
+template <class T, int ROP>
+__global__ void __launch_bounds__(RW) reduce_xgpu_emulate_kernel(const T* a, const T* b,
+                                                                  EmuShards sh, int64_t tpr,
+                                                                  P<T>* tiles, unsigned* counters,
+                                                                  T* outs, XArgs base,
+                                                                  int* status) {
+  const int r = (int)(blockIdx.x / tpr);
+  const int64_t t = blockIdx.x % tpr;
+  const int64_t n = sh.n[r];
+  const int64_t nt = (n + Geo<T>::L - 1) / Geo<T>::L;
+  XArgs x = base;
+  x.rank = r;
+  T* out = outs + 2 * r;
+  if (n == 0) {  // an empty shard still takes part in the exchange
+    if (t == 0 && threadIdx.x == 0) {
+      out[0] = T(0);
+      out[1] = T(0);
+      xgpu_exchange(out, x, status);
+    }
+    return;
+  }
+  if (t >= nt) return;
+  if (reduce_tile<T, ROP, false>(a + sh.lo[r], b + sh.lo[r], n, nt, tiles + r * tpr,
+                                 counters + r, out, t) &&
+      threadIdx.x == 0)
     xgpu_exchange(out, x, status);
 }
 
@@ -233,6 +272,82 @@ extern "C" int tf_xgpu_reduce(int rop, int dtype, int64_t n, const void* a, cons
   switch (rop) { XR(TF_RSUM) XR(TF_RSUM2) XR(TF_RDOT) }
 #undef XR
   return launch_status("tf_xgpu_reduce");
+}
+
+// Test entry: the fused reduce + exchange for `world` emulated ranks on this
+// GPU.  Rank r's shard is the next counts[r] elements of the device planes a
+// (and b); outs (device, world x 2) receives every rank's global result.
+// Synchronous.
+extern "C" int tf_xgpu_reduce_emulate(int rop, int dtype, int world, const void* a,
+                                      const void* b, const int64_t* counts, void* outs,
+                                      void* stream) {
+  if (rop < 0 || rop >= TF_NUM_ROPS || (dtype != TF_F32 && dtype != TF_F64) || world < 1 ||
+      world > XG_MAXG || !counts || !outs || !a || (rop != TF_RSUM && !b))
+    return fail(TF_EINVAL, "tf_xgpu_reduce_emulate: bad arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  const int64_t L = dtype == TF_F64 ? Geo<double>::L : Geo<float>::L;
+  EmuShards sh{};
+  int64_t off = 0, tpr = 1;
+  XArgs x{};
+  for (int r = 0; r < world; r++) {
+    if (counts[r] < 0) return fail(TF_EINVAL, "tf_xgpu_reduce_emulate: negative count");
+    sh.lo[r] = off;
+    sh.n[r] = counts[r];
+    off += counts[r];
+    const int64_t nt = (counts[r] + L - 1) / L;
+    if (nt > tpr) tpr = nt;
+    if (counts[r] > 0) {
+      if (r < 32) x.nonempty_lo |= 1ull << r;
+      else x.nonempty_hi |= 1ull << (r - 32);
+    }
+  }
+  if (tpr * world > 0x7fffffffLL) return fail(TF_EINVAL, "tf_xgpu_reduce_emulate: too large");
+  Slot* boxes = nullptr;
+  void* tiles = nullptr;
+  unsigned* counters = nullptr;
+  int* status = nullptr;
+  const size_t bbytes = sizeof(Slot) * 2 * XG_MAXG * world;
+  cudaError_t e = cudaMalloc(&boxes, bbytes);
+  if (e == cudaSuccess) e = cudaMemset(boxes, 0xff, bbytes);
+  if (e == cudaSuccess) e = cudaMalloc(&tiles, (size_t)world * tpr * 2 * tsz);
+  if (e == cudaSuccess) e = cudaMalloc(&counters, sizeof(unsigned) * world);
+  if (e == cudaSuccess) e = cudaMemset(counters, 0, sizeof(unsigned) * world);
+  if (e == cudaSuccess) e = cudaMalloc(&status, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(status, 0, sizeof(int));
+  int rc = e == cudaSuccess ? TF_OK : cuda_status(e, "tf_xgpu_reduce_emulate");
+  if (!rc) {
+    for (int r = 0; r < world; r++) x.box[r] = boxes + (size_t)r * 2 * XG_MAXG;
+    x.world = world;
+    x.epoch = 1;
+    const unsigned grid = (unsigned)(tpr * world);
+#define XE(ROP)                                                                               \
+  case ROP:                                                                                   \
+    if (dtype == TF_F64)                                                                      \
+      reduce_xgpu_emulate_kernel<double, ROP><<<grid, RW, 0, s>>>(                            \
+          static_cast<const double*>(a), static_cast<const double*>(b ? b : a), sh, tpr,      \
+          static_cast<P<double>*>(tiles), counters, static_cast<double*>(outs), x, status);   \
+    else                                                                                      \
+      reduce_xgpu_emulate_kernel<float, ROP><<<grid, RW, 0, s>>>(                             \
+          static_cast<const float*>(a), static_cast<const float*>(b ? b : a), sh, tpr,        \
+          static_cast<P<float>*>(tiles), counters, static_cast<float*>(outs), x, status);     \
+    break;
+    switch (rop) { XE(TF_RSUM) XE(TF_RSUM2) XE(TF_RDOT) }
+#undef XE
+    rc = launch_status("tf_xgpu_reduce_emulate");
+  }
+  int h = 0;
+  if (!rc) {
+    e = cudaMemcpyAsync(&h, status, sizeof h, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) rc = cuda_status(e, "tf_xgpu_reduce_emulate");
+  }
+  cudaFree(boxes);
+  cudaFree(tiles);
+  cudaFree(counters);
+  cudaFree(status);
+  if (!rc && h) rc = fail(TF_ECUDA, "tf_xgpu_reduce_emulate: exchange timed out");
+  return rc;
 }
 
 // 0 = OK, 1 = a combine timed out waiting for a peer (synchronous read).

@@ -386,6 +386,40 @@ def test_p2p_fused_reduce_single_rank_matches_reduction():
     assert tp.status() == 0
 
 
+@pytest.mark.parametrize("world", [2, 3, 4, 7, 8, 16])
+@pytest.mark.parametrize("rop", ["sum", "sum2", "dot"])
+def test_p2p_fused_reduce_emulated_ranks_match_one_gpu(world, rop):
+    # the fused reduce + exchange for `world` ranks as one grid on this GPU
+    # (tf_xgpu_reduce_emulate): shards cut by dist.shard_tiles (complete
+    # subtrees, trailing ranks possibly empty); every rank must end with the
+    # one-GPU reduction's bits — shard invariance through the fused kernel
+    import ctypes
+
+    from paper_1401_6235_b200 import _lib
+    from paper_1401_6235_b200 import dist as D
+    from paper_1401_6235_b200 import reduce as R
+
+    rng = np.random.default_rng(1000 + world)
+    for tdt in (torch.float64, torch.float32):
+        L = R.tile_elems(np.float64 if tdt == torch.float64 else np.float32)
+        n = 9 * L + 12345
+        x = _t(rng.uniform(-1, 1, n) * np.exp2(rng.integers(-25, 26, n))).to(tdt)
+        y = _t(rng.uniform(-1, 1, n)).to(tdt)
+        ref = {"sum": lambda: R.vtsum(x), "sum2": lambda: R.vtsum2((x, y)),
+               "dot": lambda: R.vtdot(x, y)}[rop]()
+        counts = D.shard_counts(n, world, L)
+        outs = torch.empty((world, 2), dtype=tdt, device=DEV)
+        c = (ctypes.c_int64 * world)(*counts)
+        dt = _lib.TF_F64 if tdt == torch.float64 else _lib.TF_F32
+        rc = _lib.lib().tf_xgpu_reduce_emulate(_lib.ROP_IDS[rop], dt, world, x.data_ptr(),
+                                               None if rop == "sum" else y.data_ptr(), c,
+                                               outs.data_ptr(),
+                                               torch.cuda.current_stream().cuda_stream)
+        _lib.check(rc, "tf_xgpu_reduce_emulate")
+        for r, (v0, v1) in enumerate(outs.cpu().tolist()):
+            assert (v0, v1) == (ref.value, ref.error), (world, rop, tdt, r, counts)
+
+
 @pytest.mark.parametrize("world", [2, 3, 5, 8, 13, 64])
 @pytest.mark.parametrize("tdt", [torch.float64, torch.float32])
 def test_p2p_protocol_emulated_ranks_match_combine(world, tdt):
