@@ -124,10 +124,17 @@ struct HostPipe {
   bool ready = false;
   cudaStream_t st[MAX_SLOTS] = {};
   cudaEvent_t done[MAX_SLOTS] = {};
-  std::vector<void*> dbuf[MAX_SLOTS];  // device staging planes (grown on demand)
-  std::vector<void*> hbuf[MAX_SLOTS];  // pinned staging for pageable planes (lazy)
+  // per slot: one device arena and one pinned arena (pageable planes only),
+  // carved per call into NP plane buffers of `plane` bytes; grown on demand
+  void* darena[MAX_SLOTS] = {};
+  void* harena[MAX_SLOTS] = {};
+  size_t dcap = 0, hcap = 0;
   CopyPool* pool = nullptr;
 };
+// Staging memory a call may use across all slots (device; the same again in
+// pinned host memory for pageable planes): a batch of many ops gets shorter
+// chunks instead of NP x 32 MB x slots of staging.
+constexpr int64_t STAGING_BUDGET = 3ll << 30;
 static HostPipe g_pipe[64];
 
 static int pipe_init(HostPipe& p) {
@@ -149,22 +156,47 @@ static int pipe_init(HostPipe& p) {
   return TF_OK;
 }
 
-static int ensure_planes(HostPipe& p, int planes, bool pinned_staging) {
-  for (int s = 0; s < p.slots; s++) {
-    while ((int)p.dbuf[s].size() < planes) {
-      void* d = nullptr;
-      cudaError_t e = cudaMalloc(&d, p.chunk_bytes);
+// Bytes per plane per slot for a call staging NP planes: the configured chunk,
+// shortened (4 KB multiples) so that NP planes x slots fit the staging budget.
+static int64_t plane_bytes(const HostPipe& p, int NP) {
+  int64_t b = STAGING_BUDGET / ((int64_t)NP * p.slots);
+  if (b > p.chunk_bytes) b = p.chunk_bytes;
+  b &= ~int64_t(4095);
+  return b < 4096 ? 4096 : b;
+}
+
+// Grow the slot arenas to hold `need` bytes each (calls are synchronous and
+// serialised by p.mu, so nothing is in flight when an arena is replaced).
+static int ensure_arenas(HostPipe& p, size_t need, bool pinned_staging) {
+  if (p.dcap < need) {
+    for (int s = 0; s < p.slots; s++) {
+      if (p.darena[s]) cudaFree(p.darena[s]);
+      p.darena[s] = nullptr;
+    }
+    p.dcap = 0;
+    for (int s = 0; s < p.slots; s++) {
+      cudaError_t e = cudaMalloc(&p.darena[s], need);
       if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: staging alloc");
-      p.dbuf[s].push_back(d);
     }
-    while (pinned_staging && (int)p.hbuf[s].size() < planes) {
-      void* h = nullptr;
-      cudaError_t e = cudaHostAlloc(&h, p.chunk_bytes, cudaHostAllocPortable);
-      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: pinned staging alloc");
-      p.hbuf[s].push_back(h);
-    }
+    p.dcap = need;
   }
-  if (pinned_staging && !p.pool) {
+  if (pinned_staging && p.hcap < need) {
+    for (int s = 0; s < p.slots; s++) {
+      if (p.harena[s]) cudaFreeHost(p.harena[s]);
+      p.harena[s] = nullptr;
+    }
+    p.hcap = 0;
+    for (int s = 0; s < p.slots; s++) {
+      cudaError_t e = cudaHostAlloc(&p.harena[s], need, cudaHostAllocPortable);
+      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise_host: pinned staging alloc");
+    }
+    p.hcap = need;
+  }
+  return TF_OK;
+}
+
+static int ensure_pool(HostPipe& p) {
+  if (!p.pool) {
     unsigned hw = std::thread::hardware_concurrency();
     int nt = hw ? (int)hw : 4;
     if (const char* v = getenv("TF_HOST_THREADS")) nt = atoi(v) > 0 ? atoi(v) : nt;
@@ -257,9 +289,13 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
   bool any_pageable = false;
   for (int q = 0; q < U; q++) any_pageable |= !(pin_in[q] = is_pinned(uniq[q]));
   for (int o = 0; o < 2 * nops; o++) any_pageable |= !(pin_out[o] = is_pinned(out[o]));
-  if ((rc = ensure_planes(p, NP, any_pageable))) return rc;
+  const int64_t pb = plane_bytes(p, NP);
+  if ((rc = ensure_arenas(p, (size_t)pb * NP, any_pageable))) return rc;
+  if (any_pageable && (rc = ensure_pool(p))) return rc;
+  auto dplane = [&](int s, int q) { return static_cast<char*>(p.darena[s]) + (size_t)q * pb; };
+  auto hplane = [&](int s, int q) { return static_cast<char*>(p.harena[s]) + (size_t)q * pb; };
 
-  const int64_t chunk = p.chunk_bytes / (int64_t)tsz;
+  const int64_t chunk = pb / (int64_t)tsz;
   const int64_t nchunks = (n + chunk - 1) / chunk;
   const int S = p.slots;
   std::vector<int64_t> slot_off(S, -1);  // chunk offset in flight in each slot
@@ -272,7 +308,7 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
     const int64_t m = (n - off) < chunk ? (n - off) : chunk;
     for (int o = 0; o < 2 * nops; o++)
       if (!pin_out[o])
-        par_memcpy(*p.pool, static_cast<char*>(out[o]) + off * tsz, p.hbuf[s][U + o],
+        par_memcpy(*p.pool, static_cast<char*>(out[o]) + off * tsz, hplane(s, U + o),
                    (size_t)m * tsz);
     slot_off[s] = -1;
     return TF_OK;
@@ -288,23 +324,23 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
     for (int q = 0; q < U; q++) {
       const void* src = static_cast<const char*>(uniq[q]) + off * tsz;
       if (!pin_in[q]) {
-        par_memcpy(*p.pool, p.hbuf[s][q], src, bytes);
-        src = p.hbuf[s][q];
+        par_memcpy(*p.pool, hplane(s, q), src, bytes);
+        src = hplane(s, q);
       }
-      cudaError_t e = cudaMemcpyAsync(p.dbuf[s][q], src, bytes, cudaMemcpyHostToDevice, st);
+      cudaError_t e = cudaMemcpyAsync(dplane(s, q), src, bytes, cudaMemcpyHostToDevice, st);
       if (e != cudaSuccess) return cuda_status(e, who);
     }
     for (int o = 0; o < nops; o++) {
       const void* din[4] = {nullptr, nullptr, nullptr, nullptr};
       for (int k = 0; k < 4; k++)
-        if (idx[4 * o + k] >= 0) din[k] = p.dbuf[s][idx[4 * o + k]];
-      void* dout[2] = {p.dbuf[s][U + 2 * o], p.dbuf[s][U + 2 * o + 1]};
+        if (idx[4 * o + k] >= 0) din[k] = dplane(s, idx[4 * o + k]);
+      void* dout[2] = {dplane(s, U + 2 * o), dplane(s, U + 2 * o + 1)};
       rc = launch ? (*launch)(o, m, din, dout, st) : ew_launch(ops[o], dtype, m, din, dout, st);
       if (rc) return rc;
     }
     for (int o = 0; o < 2 * nops; o++) {
-      void* dst = pin_out[o] ? static_cast<char*>(out[o]) + off * tsz : p.hbuf[s][U + o];
-      cudaError_t e = cudaMemcpyAsync(dst, p.dbuf[s][U + o], bytes, cudaMemcpyDeviceToHost, st);
+      void* dst = pin_out[o] ? static_cast<char*>(out[o]) + off * tsz : hplane(s, U + o);
+      cudaError_t e = cudaMemcpyAsync(dst, dplane(s, U + o), bytes, cudaMemcpyDeviceToHost, st);
       if (e != cudaSuccess) return cuda_status(e, who);
     }
     cudaError_t e = cudaEventRecord(p.done[s], st);
@@ -484,7 +520,7 @@ static int reduce_host_batch(int nred, const int* rops, int dtype, int64_t n,
       R.h[s].push_back(h);
     }
   }
-  if (pageable && (rc = ensure_planes(p, 0, true))) return rc;  // the copy pool
+  if (pageable && (rc = ensure_pool(p))) return rc;  // the copy pool
 
   void* parts = nullptr;  // nred x nchunks x 2 of dtype, then nred result pairs
   cudaError_t e = cudaMalloc(&parts, (size_t)nred * (nchunks + 1) * 2 * tsz);

@@ -338,6 +338,27 @@ def test_host_batch_matches_oracle_and_rejects_chains(oracle):
         K.host_batch([("vtadd2", X, Y, outs[0]), ("vtmul2", outs[0], Y, outs[1])])
 
 
+def test_host_batch_of_64_ops_uses_short_chunks(oracle):
+    # 64 ops = 132 staged planes: the pipeline shortens its chunks to stay in the
+    # staging budget (several chunks per plane here) — bits must not change
+    from paper_1401_6235_b200 import kernels as K
+
+    n = (1 << 20) + 3
+    a = _config2_inputs("vtadd2", n, 81)
+    X, Y = K.TwofoldArray(a[0], a[1]), K.TwofoldArray(a[2], a[3])
+    names = ["vtadd2", "vtsub2", "vtmul2", "vtdiv2", "vpadd2", "vpsub2", "vpmul2", "vpdiv2"]
+    calls, outs = [], []
+    for k in range(64):
+        o = K.empty_twofold(n, np.float64, device="cpu")
+        outs.append(o)
+        calls.append((names[k % len(names)], X, Y, o))
+    K.host_batch(calls)
+    want = {name: oracle.elementwise(name, *a) for name in names}
+    for k, o in enumerate(outs):
+        w0, w1 = want[names[k % len(names)]]
+        assert bits_equal(o.value, w0) and bits_equal(o.error, w1), k
+
+
 @pytest.mark.parametrize("fmt", ["f64", "f32"])
 def test_all_ops_on_random_bit_patterns(oracle, fmt):
     # every IEEE class (subnormals, infinities, NaNs, signed zeros, huge/tiny
