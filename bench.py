@@ -16,11 +16,14 @@ Keys beyond the base contract:
                 MEASURED_PEAKS.json hbm_gbs (burst copy figure)
   cpu_baseline  the CPU oracle port (oracle/, all host threads) on a bounded
                 sample of the same workload, rank 0 at N=1 only
-  e2e           the same metric through the public API with pinned HOST planes
-                (kernels.vtadd2(numpy...) -> tf_elementwise_host), H2D and D2H inside,
-                on the first 2^27 elements of each plane (PCIe-bound rate); its
-                roofline is the live-measured host link for the step's traffic mix;
-                e2e.batched = the same step as one kernels.host_batch call
+  e2e           the same metric through the public API with pinned HOST planes,
+                H2D and D2H inside, on the first 2^27 elements of each plane
+                (PCIe-bound rate): the step as ONE kernels.host_batch call
+                (tf_elementwise_host_batch: each distinct input plane crosses the
+                link once, every output plane comes back); e2e.per_call = the
+                reference's convention, one kernels.vtXXX(numpy...) call per op
+                (tf_elementwise_host).  Each carries a roofline against the
+                live-measured host link for its traffic mix
   per_op        per-kernel CUDA-event times and GB/s
   clocks        NVML SM clock + event reasons sampled during the timed region
 
@@ -654,30 +657,41 @@ def run_elementwise(args, rank, world, local):
             KM.host_batch(batch)
         dtb = max_over_ranks(time.perf_counter() - t0, world)
         link = link_probe()
-        hb = sum(op.h2d for op in ops) * args.e2e_steps
-        db = sum(op.d2h for op in ops) * args.e2e_steps
-        # time bound of the link for this traffic mix: each direction alone, and
-        # both together against the measured duplex total
-        t_bound = max(hb / (link["h2d"] * 1e9), db / (link["d2h"] * 1e9),
-                      (hb + db) / (link["duplex"] * 1e9))
         ne = min(n, E2E_MAX)
         e2e_units = len(ops) * ne
-        e2e = {"value": world * e2e_units * args.e2e_steps / dt, "unit": "elem-ops/s",
+
+        def link_roofline(h2d, d2h, dt):
+            # time bound of the link for this traffic mix: each direction alone,
+            # and both together against the measured duplex total
+            hb, db = h2d * args.e2e_steps, d2h * args.e2e_steps
+            t_bound = max(hb / (link["h2d"] * 1e9), db / (link["d2h"] * 1e9),
+                          (hb + db) / (link["duplex"] * 1e9))
+            return {"bound": "pcie", "achieved": (hb + db) / dt / 1e9,
+                    "peak": (hb + db) / t_bound / 1e9, "unit": "GB/s",
+                    "frac": t_bound / dt, "link_gbs": link,
+                    "peak_source": "measured live: pinned H2D, D2H and concurrent copies; "
+                                   "peak = this step's H2D/D2H mix at the link bound"}
+
+        d2h = sum(op.d2h for op in ops)
+        h2d_call = sum(op.h2d for op in ops)
+        h2d_batch = len(ps.cache) * esz * ne
+        # headline: the step as ONE public-API call over host planes (every op
+        # computed, every output plane returned; each distinct input plane
+        # crosses the link once).  per_call: the reference's calling
+        # convention, one kernels.<op>(numpy...) call per op.
+        e2e = {"value": world * e2e_units * args.e2e_steps / dtb, "unit": "elem-ops/s",
                "elems_per_op": ne,
-               "roofline": {"bound": "pcie", "achieved": (hb + db) / dt / 1e9,
-                            "peak": (hb + db) / t_bound / 1e9, "unit": "GB/s",
-                            "frac": t_bound / dt, "link_gbs": link,
-                            "peak_source": "measured live: pinned H2D, D2H and concurrent copies; "
-                                           "peak = this step's H2D/D2H mix at the link bound"},
-               "batched": {"value": world * e2e_units * args.e2e_steps / dtb,
-                           "path": "kernels.host_batch([...5 calls...]): one pipelined pass, "
-                                   "distinct host planes cross the link once",
-                           "h2d_bytes_per_step": len(ps.cache) * esz * ne},
-               "h2d_bytes_per_step": sum(op.h2d for op in ops),
-               "d2h_bytes_per_step": sum(op.d2h for op in ops),
+               "h2d_bytes_per_step": h2d_batch, "d2h_bytes_per_step": d2h,
+               "roofline": link_roofline(h2d_batch, d2h, dtb),
                "steps": args.e2e_steps,
-               "path": "kernels.<op>(pinned numpy planes) -> tf_elementwise_host "
-                       "(chunked H2D / kernel / D2H pipeline)"}
+               "path": "kernels.host_batch([(op, x, y, out) for the %d ops]) on pinned numpy "
+                       "planes -> tf_elementwise_host_batch (one chunked H2D / kernels / D2H "
+                       "pipeline)" % len(ops),
+               "per_call": {"value": world * e2e_units * args.e2e_steps / dt,
+                            "h2d_bytes_per_step": h2d_call, "d2h_bytes_per_step": d2h,
+                            "roofline": link_roofline(h2d_call, d2h, dt),
+                            "path": "kernels.<op>(pinned numpy planes) per op -> "
+                                    "tf_elementwise_host (chunked H2D / kernel / D2H pipeline)"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -837,13 +851,16 @@ def run_config4(args, rank, world, local):
             "roofline": {"bound": "hbm", "kernel": "vtdot", "achieved": gbs, "peak": peak,
                          "unit": "GB/s", "frac": gbs / peak, "traffic": ncu_traffic("vtdot"),
                          "algorithmic_bytes": 16 * n, "peak_source": src},
-            "e2e": {"value": world * 2 * n * args.e2e_steps / dt, "unit": "elem-ops/s",
-                    "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 32,
-                    "path": "reduce.vtdot / vtsum on pinned numpy planes -> tf_reduce_host",
-                    "batched": {"value": world * 2 * n * args.e2e_steps / dtb,
-                                "path": "reduce.host_batch([vtdot(x, y), vtsum(x)]): one pass, "
-                                        "x crosses the link once (tf_reduce_host_batch)",
-                                "h2d_bytes_per_step": 16 * n}},
+            # headline: the step as ONE public-API pass (x crosses the link once);
+            # per_call: one reduce.vtdot / reduce.vtsum call each
+            "e2e": {"value": world * 2 * n * args.e2e_steps / dtb, "unit": "elem-ops/s",
+                    "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 32,
+                    "path": "reduce.host_batch([vtdot(x, y), vtsum(x)]) on pinned numpy planes "
+                            "-> tf_reduce_host_batch (one pass, x crosses the link once)",
+                    "per_call": {"value": world * 2 * n * args.e2e_steps / dt,
+                                 "path": "reduce.vtdot / vtsum on pinned numpy planes -> "
+                                         "tf_reduce_host",
+                                 "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 32}},
             "cpu_baseline": cpu,
             "gpu_launches": world * K * (2 + (2 if world > 1 and tp is None else 0)),
             "reduce_transport": args.reduce_transport if world > 1 else "none (1 GPU)",

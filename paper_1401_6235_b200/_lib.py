@@ -60,6 +60,10 @@ def _bind(L: ctypes.CDLL) -> None:
         "tf_xgpu_reduce": (ci, [ci, ci, i64, vp, vp, vp, vp, ctypes.c_size_t,
                                 ctypes.POINTER(i64), vp]),
         "tf_xgpu_reduce_emulate": (ci, [ci, ci, ci, vp, vp, ctypes.POINTER(i64), vp, vp]),
+        "tf_xgpu_publish": (ci, [ci, vp, ctypes.POINTER(i64), vp]),
+        "tf_xgpu_reduce_publish": (ci, [ci, ci, i64, vp, vp, vp, vp, ctypes.c_size_t,
+                                        ctypes.POINTER(i64), vp]),
+        "tf_xgpu_collect": (ci, [ci, vp, vp]),
         "tf_horner": (ci, [ci, i64, vp, ctypes.POINTER(cd), ci, vp, vp, vp]),
         "tf_horner_host": (ci, [ci, i64, vp, ctypes.POINTER(cd), ci, vp, vp, ci]),
         "tf_fill": (ci, [ci, ci, i64, ctypes.c_uint64, i64, cd, cd, vp, vp, vp]),
@@ -78,7 +82,8 @@ EXPORTS = (
     "tf_elementwise_host", "tf_elementwise_host_batch", "tf_host_register", "tf_host_unregister", "tf_elementwise_il", "tf_fused", "tf_interleave", "tf_deinterleave",
     "tf_reduce_geometry", "tf_reduce_workspace_bytes", "tf_reduce",
     "tf_combine", "tf_reduce_host", "tf_reduce_host_batch", "tf_xgpu_mailbox", "tf_xgpu_open", "tf_xgpu_combine",
-    "tf_xgpu_status", "tf_xgpu_emulate", "tf_xgpu_reduce", "tf_xgpu_reduce_emulate", "tf_horner", "tf_horner_host", "tf_fill", "tf_dotted", "tf_fp64_peak", "tf_gen_dot_host",
+    "tf_xgpu_status", "tf_xgpu_emulate", "tf_xgpu_reduce", "tf_xgpu_reduce_emulate",
+    "tf_xgpu_publish", "tf_xgpu_reduce_publish", "tf_xgpu_collect", "tf_horner", "tf_horner_host", "tf_fill", "tf_dotted", "tf_fp64_peak", "tf_gen_dot_host",
 )
 
 

@@ -30,10 +30,22 @@
 
 namespace tf {
 
+// The split (two-phase) form: XM_PUBLISH stores this rank's partial and flags
+// and returns; XM_COLLECT later waits for and folds the peers'.  The caller
+// orders the phases across ranks (a host barrier in between), so no kernel
+// ever waits on another rank's kernel.
+enum { XM_FULL = 0, XM_PUBLISH = 1, XM_COLLECT = 2 };
+
 template <class T>
-__global__ void xgpu_exchange_kernel(T* out, XArgs x, int* status) {
+__device__ __forceinline__ void xgpu_run(T* out, const XArgs& x, int* status, int mode) {
+  if (mode != XM_COLLECT) xgpu_publish(out, x);
+  if (mode != XM_PUBLISH) xgpu_collect(out, x, status);
+}
+
+template <class T>
+__global__ void xgpu_exchange_kernel(T* out, XArgs x, int* status, int mode) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  xgpu_exchange(out, x, status);
+  xgpu_run(out, x, status, mode);
 }
 
 // Reduction fused with the exchange: every CTA reduces its tile as in
@@ -45,10 +57,10 @@ __global__ void __launch_bounds__(RW) reduce_xgpu_kernel(const T* __restrict__ a
                                                          const T* __restrict__ b, int64_t n,
                                                          int64_t ntiles, P<T>* tiles,
                                                          unsigned* counter, T* out, XArgs x,
-                                                         int* status) {
+                                                         int* status, int mode) {
   if (reduce_tile<T, ROP, VEC>(a, b, n, ntiles, tiles, counter, out, blockIdx.x) &&
       threadIdx.x == 0)
-    xgpu_exchange(out, x, status);
+    xgpu_run(out, x, status, mode);
 }
 
 // One-GPU emulation of the FUSED path for `world` ranks: one grid, tpr CTAs per
@@ -115,6 +127,8 @@ struct XCtx {
   int rank = -1, world = 0;
   unsigned long long epoch = 0;
   int* status = nullptr;
+  XArgs published{};  // the exchange a split-form publish left for its collect
+  bool pending = false;
 };
 static XCtx g_x[64];
 
@@ -194,29 +208,17 @@ extern "C" int tf_xgpu_open(int device, int world, int rank, const void* handles
   return TF_OK;
 }
 
-// Exchange + combine: out (device, 2 x dtype) holds this rank's partial on entry
-// and the global result on exit.  counts: host array of world shard sizes.
-extern "C" int tf_xgpu_combine(int dtype, void* out, const int64_t* counts, void* stream) {
-  XCtx* c = ctx_for_current(nullptr);
-  if (!c || c->world < 1) return fail(TF_EINVAL, "tf_xgpu_combine: transport not open");
-  if ((dtype != TF_F32 && dtype != TF_F64) || !out || !counts)
-    return fail(TF_EINVAL, "tf_xgpu_combine: bad arguments");
-  std::lock_guard<std::mutex> lock(c->mu);
-  XArgs x = next_exchange(*c, counts);
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (dtype == TF_F64)
-    xgpu_exchange_kernel<double><<<1, 32, 0, s>>>(static_cast<double*>(out), x, c->status);
-  else
-    xgpu_exchange_kernel<float><<<1, 32, 0, s>>>(static_cast<float*>(out), x, c->status);
-  return launch_status("tf_xgpu_combine");
-}
-
 namespace tf {
 size_t reduce_ws_bytes(int dtype, int64_t n);
 
+template <class T>
+static void launch_exchange(void* out, const XArgs& x, int* status, int mode, cudaStream_t s) {
+  xgpu_exchange_kernel<T><<<1, 32, 0, s>>>(static_cast<T*>(out), x, status, mode);
+}
+
 template <class T, int ROP>
 static void launch_reduce_xgpu(int64_t n, const void* a, const void* b, void* out, void* ws,
-                               const XArgs& x, int* status, cudaStream_t s) {
+                               const XArgs& x, int* status, int mode, cudaStream_t s) {
   const int64_t nt = (n + Geo<T>::L - 1) / Geo<T>::L;
   unsigned* counter = static_cast<unsigned*>(ws);
   P<T>* tiles = reinterpret_cast<P<T>*>(static_cast<char*>(ws) + 256);
@@ -225,12 +227,84 @@ static void launch_reduce_xgpu(int64_t n, const void* a, const void* b, void* ou
   T* po = static_cast<T*>(out);
   if (aligned16(a) && (ROP == TF_RSUM || aligned16(b)))
     reduce_xgpu_kernel<T, ROP, true><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
-                                                                 po, x, status);
+                                                                 po, x, status, mode);
   else
     reduce_xgpu_kernel<T, ROP, false><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles, counter,
-                                                                  po, x, status);
+                                                                  po, x, status, mode);
+}
+
+// The epoch of a new exchange (caller holds c.mu).  A split-form publish leaves
+// it pending until tf_xgpu_collect; nothing else may start in between.
+static int begin_exchange(XCtx& c, const int64_t* counts, int mode, const char* who,
+                          XArgs* x) {
+  if (c.pending)
+    return fail(TF_EINVAL, std::string(who) + ": a published exchange awaits tf_xgpu_collect");
+  *x = next_exchange(c, counts);
+  if (mode == XM_PUBLISH) {
+    c.published = *x;
+    c.pending = true;
+  }
+  return TF_OK;
+}
+
+static int xgpu_combine_impl(int dtype, void* out, const int64_t* counts, void* stream, int mode,
+                             const char* who) {
+  XCtx* c = ctx_for_current(nullptr);
+  if (!c || c->world < 1) return fail(TF_EINVAL, std::string(who) + ": transport not open");
+  if ((dtype != TF_F32 && dtype != TF_F64) || !out || !counts)
+    return fail(TF_EINVAL, std::string(who) + ": bad arguments");
+  std::lock_guard<std::mutex> lock(c->mu);
+  XArgs x;
+  if (int rc = begin_exchange(*c, counts, mode, who, &x)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == TF_F64) launch_exchange<double>(out, x, c->status, mode, s);
+  else launch_exchange<float>(out, x, c->status, mode, s);
+  return launch_status(who);
+}
+
+static int xgpu_reduce_impl(int rop, int dtype, int64_t n, const void* a, const void* b,
+                            void* out, void* ws, size_t ws_bytes, const int64_t* counts,
+                            void* stream, int mode, const char* who) {
+  const std::string w(who);
+  XCtx* c = ctx_for_current(nullptr);
+  if (!c || c->world < 1) return fail(TF_EINVAL, w + ": transport not open");
+  if (rop < 0 || rop >= TF_NUM_ROPS) return fail(TF_EINVAL, w + ": unknown reduction id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, w + ": planes must be float32 or float64");
+  if (n < 0 || !out || !counts) return fail(TF_EINVAL, w + ": bad arguments");
+  if (n > 0 && (!a || (rop != TF_RSUM && !b))) return fail(TF_EINVAL, w + ": null plane");
+  if (n > 0 && (!ws || ws_bytes < reduce_ws_bytes(dtype, n)))
+    return fail(TF_EINVAL, w + ": workspace too small");
+  const int64_t L = dtype == TF_F64 ? Geo<double>::L : Geo<float>::L;
+  if ((n + L - 1) / L > 0x7fffffffLL) return fail(TF_EINVAL, w + ": too many tiles");
+  std::lock_guard<std::mutex> lock(c->mu);
+  XArgs x;
+  if (int rc = begin_exchange(*c, counts, mode, who, &x)) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  if (n == 0) {  // nothing to reduce: (+0, +0), skipped by the fold (count 0)
+    cudaError_t e = cudaMemsetAsync(out, 0, 2 * tsz, s);
+    if (e != cudaSuccess) return cuda_status(e, who);
+    if (dtype == TF_F64) launch_exchange<double>(out, x, c->status, mode, s);
+    else launch_exchange<float>(out, x, c->status, mode, s);
+    return launch_status(who);
+  }
+#define XR(ROP)                                                                                   \
+  case ROP:                                                                                       \
+    if (dtype == TF_F64) launch_reduce_xgpu<double, ROP>(n, a, b, out, ws, x, c->status, mode, s); \
+    else launch_reduce_xgpu<float, ROP>(n, a, b, out, ws, x, c->status, mode, s);                 \
+    break;
+  switch (rop) { XR(TF_RSUM) XR(TF_RSUM2) XR(TF_RDOT) }
+#undef XR
+  return launch_status(who);
 }
 }  // namespace tf
+
+// Exchange + combine: out (device, 2 x dtype) holds this rank's partial on entry
+// and the global result on exit.  counts: host array of world shard sizes.
+extern "C" int tf_xgpu_combine(int dtype, void* out, const int64_t* counts, void* stream) {
+  return xgpu_combine_impl(dtype, out, counts, stream, XM_FULL, "tf_xgpu_combine");
+}
 
 // Reduce this rank's shard AND exchange/combine over NVLink in one launch:
 // tf_reduce followed by tf_xgpu_combine, fused (the last CTA publishes the local
@@ -240,38 +314,41 @@ static void launch_reduce_xgpu(int64_t n, const void* a, const void* b, void* ou
 extern "C" int tf_xgpu_reduce(int rop, int dtype, int64_t n, const void* a, const void* b,
                               void* out, void* ws, size_t ws_bytes, const int64_t* counts,
                               void* stream) {
+  return xgpu_reduce_impl(rop, dtype, n, a, b, out, ws, ws_bytes, counts, stream, XM_FULL,
+                          "tf_xgpu_reduce");
+}
+
+// Split form, phase 1: as tf_xgpu_combine / tf_xgpu_reduce, but the device
+// thread only publishes this rank's partial (data, fence, epoch flags) and
+// returns; out keeps the local partial.  Once the caller knows every rank's
+// publish has completed (e.g. stream sync + host barrier), tf_xgpu_collect
+// waits for nothing and folds.  No kernel ever waits on another rank's kernel,
+// so ranks may even share one GPU (how the IPC mapping is tested here).
+extern "C" int tf_xgpu_publish(int dtype, void* out, const int64_t* counts, void* stream) {
+  return xgpu_combine_impl(dtype, out, counts, stream, XM_PUBLISH, "tf_xgpu_publish");
+}
+
+extern "C" int tf_xgpu_reduce_publish(int rop, int dtype, int64_t n, const void* a,
+                                      const void* b, void* out, void* ws, size_t ws_bytes,
+                                      const int64_t* counts, void* stream) {
+  return xgpu_reduce_impl(rop, dtype, n, a, b, out, ws, ws_bytes, counts, stream, XM_PUBLISH,
+                          "tf_xgpu_reduce_publish");
+}
+
+// Split form, phase 2: fold the pending exchange's partials into out (2 x dtype,
+// device); dtype must match the publish.
+extern "C" int tf_xgpu_collect(int dtype, void* out, void* stream) {
   XCtx* c = ctx_for_current(nullptr);
-  if (!c || c->world < 1) return fail(TF_EINVAL, "tf_xgpu_reduce: transport not open");
-  if (rop < 0 || rop >= TF_NUM_ROPS) return fail(TF_EINVAL, "tf_xgpu_reduce: unknown reduction id");
-  if (dtype != TF_F32 && dtype != TF_F64)
-    return fail(TF_EINVAL, "tf_xgpu_reduce: planes must be float32 or float64");
-  if (n < 0 || !out || !counts) return fail(TF_EINVAL, "tf_xgpu_reduce: bad arguments");
-  if (n > 0 && (!a || (rop != TF_RSUM && !b))) return fail(TF_EINVAL, "tf_xgpu_reduce: null plane");
-  if (n > 0 && (!ws || ws_bytes < reduce_ws_bytes(dtype, n)))
-    return fail(TF_EINVAL, "tf_xgpu_reduce: workspace too small");
-  const int64_t L = dtype == TF_F64 ? Geo<double>::L : Geo<float>::L;
-  if ((n + L - 1) / L > 0x7fffffffLL) return fail(TF_EINVAL, "tf_xgpu_reduce: too many tiles");
+  if (!c || c->world < 1) return fail(TF_EINVAL, "tf_xgpu_collect: transport not open");
+  if ((dtype != TF_F32 && dtype != TF_F64) || !out)
+    return fail(TF_EINVAL, "tf_xgpu_collect: bad arguments");
   std::lock_guard<std::mutex> lock(c->mu);
-  XArgs x = next_exchange(*c, counts);
+  if (!c->pending) return fail(TF_EINVAL, "tf_xgpu_collect: no published exchange");
+  c->pending = false;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const size_t tsz = dtype == TF_F64 ? 8 : 4;
-  if (n == 0) {  // nothing to reduce: (+0, +0), skipped by the fold (count 0)
-    cudaError_t e = cudaMemsetAsync(out, 0, 2 * tsz, s);
-    if (e != cudaSuccess) return cuda_status(e, "tf_xgpu_reduce");
-    if (dtype == TF_F64)
-      xgpu_exchange_kernel<double><<<1, 32, 0, s>>>(static_cast<double*>(out), x, c->status);
-    else
-      xgpu_exchange_kernel<float><<<1, 32, 0, s>>>(static_cast<float*>(out), x, c->status);
-    return launch_status("tf_xgpu_reduce");
-  }
-#define XR(ROP)                                                                            \
-  case ROP:                                                                                \
-    if (dtype == TF_F64) launch_reduce_xgpu<double, ROP>(n, a, b, out, ws, x, c->status, s); \
-    else launch_reduce_xgpu<float, ROP>(n, a, b, out, ws, x, c->status, s);                 \
-    break;
-  switch (rop) { XR(TF_RSUM) XR(TF_RSUM2) XR(TF_RDOT) }
-#undef XR
-  return launch_status("tf_xgpu_reduce");
+  if (dtype == TF_F64) launch_exchange<double>(out, c->published, c->status, XM_COLLECT, s);
+  else launch_exchange<float>(out, c->published, c->status, XM_COLLECT, s);
+  return launch_status("tf_xgpu_collect");
 }
 
 // Test entry: the fused reduce + exchange for `world` emulated ranks on this

@@ -30,12 +30,13 @@ __device__ __forceinline__ P<T> xcomb(P<T> l, P<T> r) {
 
 // The protocol, for one rank; run by one thread.  Shared by the real transport
 // kernel (one rank per GPU) and the one-GPU emulation (one rank per block).
+// Phase 1 (publish): this rank's partial into every mailbox, one system fence,
+// then the epoch flags.
 template <class T>
-__device__ void xgpu_exchange(T* out, const XArgs& x, int* status) {
+__device__ void xgpu_publish(const T* out, const XArgs& x) {
   const int par = (int)(x.epoch & 1);
   const volatile T* mine_v = out;
   const double z0 = (double)mine_v[0], z1 = (double)mine_v[1];
-  // 1. publish: data everywhere, one system fence, then the flags
   for (int r = 0; r < x.world; r++) {
     volatile Slot* s = x.box[r] + par * XG_MAXG + x.rank;
     s->z0 = z0;
@@ -46,7 +47,13 @@ __device__ void xgpu_exchange(T* out, const XArgs& x, int* status) {
     volatile Slot* s = x.box[r] + par * XG_MAXG + x.rank;
     s->seq = x.epoch;
   }
-  // 2. wait for every rank's slot of this epoch in the local mailbox
+}
+
+// Phase 2 (collect): wait (bounded) for every rank's slot of this epoch in the
+// local mailbox, then fold the non-empty ranks' partials into out.
+template <class T>
+__device__ void xgpu_collect(T* out, const XArgs& x, int* status) {
+  const int par = (int)(x.epoch & 1);
   volatile Slot* mine = x.box[x.rank] + par * XG_MAXG;
   const long long t0 = clock64();
   for (int r = 0; r < x.world; r++) {
@@ -59,7 +66,7 @@ __device__ void xgpu_exchange(T* out, const XArgs& x, int* status) {
     }
   }
   __threadfence_system();
-  // 3. skip tree over the non-empty ranks, in rank order (as tf_combine)
+  // skip tree over the non-empty ranks, in rank order (as tf_combine)
   P<T> st[8];
   int lv[8];
   int sp = 0, m = 0;
@@ -87,6 +94,12 @@ __device__ void xgpu_exchange(T* out, const XArgs& x, int* status) {
   for (int s = sp - 2; s >= 0; s--) acc = xcomb(st[s], acc);
   out[0] = acc.a;
   out[1] = acc.b;
+}
+
+template <class T>
+__device__ void xgpu_exchange(T* out, const XArgs& x, int* status) {
+  xgpu_publish(out, x);
+  xgpu_collect(out, x, status);
 }
 
 }  // namespace tf

@@ -168,16 +168,43 @@ class P2PTransport:
         self._lib.check(rc, "P2PTransport.combine")
         return partial
 
-    def reduce(self, rop, planes, counts, out=None):
+    def publish(self, partial, counts):
+        """Split form, phase 1 (tf_xgpu_publish): store this rank's partial in every
+        peer's mailbox and return.  ``collect`` must follow on every rank once all
+        ranks' publishes have completed (stream sync + host barrier)."""
+        import ctypes
+
+        dt = self._lib.TF_F64 if partial.dtype == torch.float64 else self._lib.TF_F32
+        c = (ctypes.c_int64 * self.world)(*[int(v) for v in counts])
+        with torch.cuda.device(partial.device):
+            s = torch.cuda.current_stream(partial.device).cuda_stream
+            rc = self._lib.lib().tf_xgpu_publish(dt, partial.data_ptr(), c, s)
+        self._lib.check(rc, "P2PTransport.publish")
+        return partial
+
+    def collect(self, out):
+        """Split form, phase 2 (tf_xgpu_collect): fold the published partials into
+        ``out`` (2-element CUDA tensor of the published dtype)."""
+        dt = self._lib.TF_F64 if out.dtype == torch.float64 else self._lib.TF_F32
+        with torch.cuda.device(out.device):
+            s = torch.cuda.current_stream(out.device).cuda_stream
+            rc = self._lib.lib().tf_xgpu_collect(dt, out.data_ptr(), s)
+        self._lib.check(rc, "P2PTransport.collect")
+        return out
+
+    def reduce(self, rop, planes, counts, out=None, publish_only=False):
         """This rank's reduction of ``planes`` (its shard, CUDA tensors) fused with
         the exchange: ONE launch (tf_xgpu_reduce) leaves the global twofold in
-        ``out`` (a 2-element CUDA tensor; allocated if None) on the current stream."""
+        ``out`` (a 2-element CUDA tensor; allocated if None) on the current stream.
+        ``publish_only``: the split form (tf_xgpu_reduce_publish) — ``out`` gets the
+        local result, published to the peers; ``collect(out)`` finishes it."""
         import ctypes
 
         from . import reduce as R
         from .kernels import _describe, _dtype_id
 
-        ps = [_describe("P2PTransport.reduce", p) for p in planes]
+        who = "P2PTransport.reduce"
+        ps = [_describe(who, p) for p in planes]
         first = ps[0]
         if any(p.kind != "cuda" for p in ps):
             raise ValueError("P2PTransport.reduce: planes must be CUDA tensors")
@@ -191,11 +218,12 @@ class P2PTransport:
         c = (ctypes.c_int64 * self.world)(*[int(v) for v in counts])
         with torch.cuda.device(first.device):
             s = torch.cuda.current_stream(first.device).cuda_stream
-            rc = self._lib.lib().tf_xgpu_reduce(
-                self._lib.ROP_IDS[rop], dt, first.n, first.ptr,
-                ps[1].ptr if len(ps) > 1 else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
-                c, s)
-        self._lib.check(rc, "P2PTransport.reduce")
+            fn = self._lib.lib().tf_xgpu_reduce_publish if publish_only else \
+                self._lib.lib().tf_xgpu_reduce
+            rc = fn(self._lib.ROP_IDS[rop], dt, first.n, first.ptr,
+                    ps[1].ptr if len(ps) > 1 else None, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                    c, s)
+        self._lib.check(rc, who)
         return out
 
     def status(self):

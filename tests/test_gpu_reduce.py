@@ -386,6 +386,39 @@ def test_p2p_fused_reduce_single_rank_matches_reduction():
     assert tp.status() == 0
 
 
+def test_p2p_split_form_single_rank():
+    # publish / collect (tf_xgpu_publish, tf_xgpu_reduce_publish, tf_xgpu_collect):
+    # the same bits as the fused forms; one pending exchange at a time
+    from paper_1401_6235_b200 import _lib
+    from paper_1401_6235_b200 import dist as D
+    from paper_1401_6235_b200 import reduce as R
+
+    tp = D.P2PTransport()
+    rng = np.random.default_rng(11)
+    with pytest.raises(ValueError, match="no published exchange"):
+        tp.collect(torch.empty(2, dtype=torch.float64, device=DEV))
+    for trial, n in enumerate([3 * 65536 + 5, 0, 1, 70000]):
+        x = _t(rng.uniform(-1, 1, n) * np.exp2(rng.integers(-20, 21, n)))
+        y = _t(rng.uniform(-1, 1, n))
+        for rop, planes, ref in (("sum", (x,), lambda: R.vtsum(x)),
+                                 ("dot", (x, y), lambda: R.vtdot(x, y))):
+            want = ref()
+            o = tp.reduce(rop, planes, [n], publish_only=True)
+            with pytest.raises(ValueError, match="awaits tf_xgpu_collect"):
+                tp.combine(torch.zeros(2, dtype=torch.float64, device=DEV), [n])
+            local = o.cpu().tolist()  # the local result, as published
+            assert local == [want.value, want.error] or n == 0
+            tp.collect(o)
+            assert o.cpu().tolist() == [want.value, want.error], (rop, n)
+        part = torch.tensor([want.value, want.error], device=DEV).float()
+        tp.publish(part, [n])
+        tp.collect(part)
+        w32 = torch.tensor([want.value, want.error], device=DEV).float().cpu().tolist()
+        assert part.cpu().tolist() == (w32 if n else [0.0, 0.0])
+    assert tp.status() == 0
+    assert _lib.lib().tf_xgpu_collect(_lib.TF_F64, None, None) != 0  # bad arguments
+
+
 @pytest.mark.parametrize("world", [2, 3, 4, 7, 8, 16])
 @pytest.mark.parametrize("rop", ["sum", "sum2", "dot"])
 def test_p2p_fused_reduce_emulated_ranks_match_one_gpu(world, rop):
