@@ -66,6 +66,10 @@ def parse():
                     help="config4 cross-GPU combine: NCCL all-gather + tf_combine, or each "
                          "reduction fused with the NVLink peer-memory exchange in one launch "
                          "(tf_xgpu_reduce, csrc/xgpu.cu)")
+    ap.add_argument("--l2-flush", choices=["write", "write-read"], default="write-read",
+                    help="between timed steps of an L2-sized working set: write a 512 MB "
+                         "buffer, then (write-read) read another 512 MB so the flush's own "
+                         "dirty lines are written back before, not inside, the next step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26,
@@ -530,6 +534,30 @@ def run_reference_config5(args):
         ms_per_step=1e3 * dt / args.steps, data="synthetic x ~ U[0.9,1.1] (seeded numpy)")
 
 
+class L2Flush:
+    """Cold-L2 flush between timed launches (outside the timed intervals): a
+    512 MB memset (larger than the 126 MB L2); with mode write-read, then a read
+    of a second 512 MB buffer, which evicts — writes back — the memset's dirty
+    lines, so the timed kernel does not pay for the flush's write-back."""
+
+    def __init__(self, mode):
+        import torch
+
+        self.mode = mode
+        self.w = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        self.r = torch.zeros(64 << 20, dtype=torch.int64, device="cuda") \
+            if mode == "write-read" else None
+
+    def __call__(self, k):
+        self.w.fill_(k & 0xFF)
+        if self.r is not None:
+            self.r.max()
+
+    def describe(self):
+        return ("512 MB memset + 512 MB read between steps" if self.r is not None
+                else "512 MB memset between steps") + " (outside the timed intervals)"
+
+
 def run_elementwise(args, rank, world, local):
     import torch
 
@@ -563,11 +591,11 @@ def run_elementwise(args, rank, world, local):
         # small, launch-bound steps: one CUDA graph per step, replayed K times
         # (per-op times come from an eager pass with events around each launch)
         ws0 = sum(t.numel() * t.element_size() for t in ps.cache.values()) + 2 * n * esz
-        scrub0 = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if ws0 < (384 << 20) else None
+        scrub0 = L2Flush(args.l2_flush) if ws0 < (384 << 20) else None
         for s in range(K):
             for j, op in enumerate(ops):
                 if scrub0 is not None:
-                    scrub0.fill_(j & 0xFF)  # cold L2 for every timed launch
+                    scrub0(j)  # cold L2 for every timed launch
                 ev[s][j][0].record(stream)
                 op.launch()
                 ev[s][j][1].record(stream)
@@ -587,7 +615,7 @@ def run_elementwise(args, rank, world, local):
     # memset outside the timed intervals); larger ones stream from HBM anyway
     ws_bytes = sum(t.numel() * t.element_size() for t in ps.cache.values()) + 2 * n * esz
     flush = ws_bytes < (384 << 20)
-    scrub = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if flush else None
+    scrub = L2Flush(args.l2_flush) if flush else None
     step_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                for _ in range(K)]
     barrier(world)
@@ -596,7 +624,7 @@ def run_elementwise(args, rank, world, local):
         start.record(stream)
         for s in range(K):
             if flush:
-                scrub.fill_(s & 0xFF)
+                scrub(s)
             step_ev[s][0].record(stream)
             if use_graph:
                 g.replay()
@@ -723,8 +751,7 @@ def run_elementwise(args, rank, world, local):
             "data": "synthetic (seeded, device-generated with BASELINE distributions)",
             "config": {"workload": wl["desc"], "n_per_gpu": n, "ops": wl["names"],
                        "timing": "cuda-graph replay per step" if use_graph else "eager launches",
-                       "l2_flush": "512 MB memset between steps (outside the timed intervals)"
-                       if flush else None,
+                       "l2_flush": scrub.describe() if flush else None,
                        "layout": "split SoA planes",
                        "inputs": "tf_fill counter-based splitmix64 on the device; plane k seed "
                                  "1000+17k, element i of rank r is global index r*n+i",
