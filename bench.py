@@ -25,6 +25,9 @@ Keys beyond the base contract:
                 (tf_elementwise_host).  Each carries a roofline against the
                 live-measured host link for its traffic mix
   per_op        per-kernel CUDA-event times and GB/s
+  device_batch  the step's ops as ONE launch (kernels.batch -> tf_elementwise_batch):
+                each distinct input plane read from HBM once, each op into its own
+                output planes; beside the headline, which is one launch per op
   clocks        NVML SM clock + event reasons sampled during the timed region
 
 --impl reference times the reference algorithm's CPU implementation — the oracle
@@ -71,6 +74,8 @@ def parse():
                          "buffer, then (write-read) read another 512 MB so the flush's own "
                          "dirty lines are written back before, not inside, the next step")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-device-batch", action="store_true",
+                    help="skip the one-launch-per-step device batch leg (extra output planes)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26,
                     help="elements per op in the CPU baseline sample (the reference arm "
@@ -174,7 +179,66 @@ def workload_elementwise(names, dtype, n, rank, config, want_host):
                       host_call=(lambda f=spec.func, a=host_args: f(*a)) if want_host else None,
                       h2d=nin * esz * min(n, E2E_MAX), d2h=2 * esz * min(n, E2E_MAX)))
         ops[-1].host_args = host_args
+        ops[-1].planes = planes
     return ops, ps
+
+
+def _call(K, name, planes, out):
+    """(name, *args, out) in the kernel's own signature, for kernels.batch."""
+    T = K.TwofoldArray
+    arity = K.KERNELS[name].arity
+    if arity == "22":
+        return (name, T(planes[0], planes[1]), T(planes[2], planes[3]), out)
+    if arity == "21":
+        return (name, T(planes[0], planes[1]), planes[2], out)
+    if arity == "11":
+        return (name, planes[0], planes[1], out)
+    if arity == "u2":
+        return (name, T(planes[0], planes[1]), out)
+    return (name, planes[0], out)
+
+
+def device_batch_leg(args, ops, n, esz, peak, world):
+    """The step's ops as ONE launch (kernels.batch -> tf_elementwise_batch), each
+    op into its own output planes; each distinct input plane is read from HBM
+    once.  Reported beside the headline, which stays one launch per op (the
+    reference's API)."""
+    import torch
+
+    from paper_1401_6235_b200 import kernels as K
+
+    dev = torch.cuda.current_device()
+    tdt = torch.float64 if esz == 8 else torch.float32
+    outs = [K.empty_twofold(n, tdt, device=dev) for _ in ops]
+    calls = [_call(K, op.name, op.planes, o) for op, o in zip(ops, outs)]
+    distinct = {p.data_ptr() for op in ops for p in op.planes}
+    nbytes = (len(distinct) + 2 * len(ops)) * esz * n
+    stream = torch.cuda.current_stream()
+    for _ in range(max(1, args.warmup)):
+        K.batch(calls)
+    flush = (nbytes < (384 << 20))
+    scrub = L2Flush(args.l2_flush) if flush else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    barrier(world)
+    torch.cuda.synchronize()
+    for s in range(args.steps):
+        if flush:
+            scrub(s)
+        ev[s][0].record(stream)
+        K.batch(calls)
+        ev[s][1].record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), world) / args.steps
+    del outs, calls
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    return {"value": world * len(ops) * n / (ms * 1e-3), "unit": "elem-ops/s",
+            "ms_per_step": ms, "bytes_per_step": nbytes, "distinct_input_planes": len(distinct),
+            "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
+                         "frac": gbs / peak},
+            "launches_per_step": 1,
+            "path": "kernels.batch([%d calls]) -> tf_elementwise_batch: one launch per step, "
+                    "each op into its own output planes" % len(ops)}
 
 
 # --------------------------------------------------------------------------
@@ -659,6 +723,10 @@ def run_elementwise(args, rank, world, local):
     units_per_step = sum(op.units for op in ops)
     value = world * units_per_step * K / (elapsed_ms * 1e-3)
     bytes_per_step = sum(op.nbytes for op in ops)
+    dbatch = None
+    if not args.no_device_batch and len(ops) > 1:
+        log("device batch")
+        dbatch = device_batch_leg(args, ops, n, esz, peak, world)
 
     # end-to-end through the public API with pinned host planes
     e2e = None
@@ -764,6 +832,7 @@ def run_elementwise(args, rank, world, local):
             "per_op": per_op,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "device_batch": dbatch,
             "gpu_launches": launches * world,
             "clocks": clk.summary(),
         }

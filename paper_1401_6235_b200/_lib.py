@@ -42,6 +42,7 @@ def _bind(L: ctypes.CDLL) -> None:
         "tf_host_register": (ci, [vp, ctypes.c_size_t]),
         "tf_host_unregister": (ci, [vp]),
         "tf_elementwise_host_batch": (ci, [ci, ctypes.POINTER(ci), ci, i64, pvp, pvp, ci]),
+        "tf_elementwise_batch": (ci, [ci, ctypes.POINTER(ci), ci, i64, pvp, pvp, vp]),
         "tf_elementwise_il": (ci, [ci, ci, i64, vp, vp, vp, vp]),
         "tf_fused": (ci, [ci, ci, i64, pvp, pvp, vp]),
         "tf_interleave": (ci, [ci, i64, vp, vp, vp, vp]),
@@ -79,7 +80,7 @@ def _bind(L: ctypes.CDLL) -> None:
 
 EXPORTS = (
     "tf_abi_version", "tf_last_error", "tf_num_inputs", "tf_selftest", "tf_elementwise",
-    "tf_elementwise_host", "tf_elementwise_host_batch", "tf_host_register", "tf_host_unregister", "tf_elementwise_il", "tf_fused", "tf_interleave", "tf_deinterleave",
+    "tf_elementwise_host", "tf_elementwise_host_batch", "tf_elementwise_batch", "tf_host_register", "tf_host_unregister", "tf_elementwise_il", "tf_fused", "tf_interleave", "tf_deinterleave",
     "tf_reduce_geometry", "tf_reduce_workspace_bytes", "tf_reduce",
     "tf_combine", "tf_reduce_host", "tf_reduce_host_batch", "tf_xgpu_mailbox", "tf_xgpu_open", "tf_xgpu_combine",
     "tf_xgpu_status", "tf_xgpu_emulate", "tf_xgpu_reduce", "tf_xgpu_reduce_emulate",

@@ -335,21 +335,11 @@ __all__ = ["TwofoldArray", "CoupledArray", "KernelSpec", "KERNELS",
            "empty_twofold"] + [row[0] for row in _TABLE]
 
 
-def host_batch(calls, device=None):
-    """Run several kernels on host (numpy) planes in ONE pipelined pass.
-
-    ``calls`` is a list of ``(name, *args, out)`` tuples with each kernel's own
-    signature, e.g. ``[("vtadd2", x, y, o1), ("vtsqrt1", x, o2)]``.  All planes
-    share one length and dtype.  Each distinct input plane crosses the host link
-    once per chunk however many calls read it; outputs come back in call order,
-    so the results equal running the calls one by one.  No output may overlap
-    any input of the batch (an intra-batch dependency), checked before any copy.
-    """
-    import ctypes
-
-    if not calls:
-        return
-    ops, ins, outs, first = [], [], [], None
+def _parse_batch(calls, who):
+    """Validate a batch of ``(name, *args, out)`` calls (each with its kernel's own
+    signature); returns (op ids, input pointers (4 per op), output pointers (2 per
+    op), the first plane's description, every description)."""
+    ops, ins, outs, first, descs = [], [], [], None, []
     for call in calls:
         name, args = call[0], call[1:]
         spec = KERNELS[name]
@@ -369,18 +359,38 @@ def host_batch(calls, device=None):
             x, (r0, r1) = args
             planes = (x,)
         desc = _check(name, planes, (r0, r1))
-        if any(d.kind != "host" for d in desc):
-            raise ValueError("%s: host_batch takes numpy (host) planes" % name)
-        for d in desc:
-            if isinstance(d.obj, np.ndarray):
-                _maybe_register(d.obj)
         if first is None:
             first = desc[0]
-        elif desc[0].dtype != first.dtype or desc[0].n != first.n:
-            raise ValueError("%s: batch planes mix dtypes or lengths" % name)
+        elif (desc[0].dtype != first.dtype or desc[0].n != first.n
+              or desc[0].kind != first.kind or desc[0].device != first.device):
+            raise ValueError("%s: batch planes mix dtypes, lengths or devices" % name)
         ops.append(spec.core)
         ins.extend([d.ptr for d in desc[:len(planes)]] + [None] * (4 - len(planes)))
         outs.extend([d.ptr for d in desc[len(planes):]])
+        descs.extend(desc)
+    return ops, ins, outs, first, descs
+
+
+def host_batch(calls, device=None):
+    """Run several kernels on host (numpy) planes in ONE pipelined pass.
+
+    ``calls`` is a list of ``(name, *args, out)`` tuples with each kernel's own
+    signature, e.g. ``[("vtadd2", x, y, o1), ("vtsqrt1", x, o2)]``.  All planes
+    share one length and dtype.  Each distinct input plane crosses the host link
+    once per chunk however many calls read it; outputs come back in call order,
+    so the results equal running the calls one by one.  No output may overlap
+    any input of the batch (an intra-batch dependency), checked before any copy.
+    """
+    import ctypes
+
+    if not calls:
+        return
+    ops, ins, outs, first, descs = _parse_batch(calls, "host_batch")
+    if any(d.kind != "host" for d in descs):
+        raise ValueError("%s: host_batch takes numpy (host) planes" % calls[0][0])
+    for d in descs:
+        if isinstance(d.obj, np.ndarray):
+            _maybe_register(d.obj)
     # cross-call aliasing (an output of one call over an input of another) is
     # rejected by the library before any copy (TF_EINVAL -> ValueError)
     L = _lib.lib()
@@ -390,6 +400,44 @@ def host_batch(calls, device=None):
     rc = L.tf_elementwise_host_batch(len(ops), arr_ops, _dtype_id(first.dtype), first.n,
                                      _lib.ptr_array(ins), _lib.ptr_array(outs), dev)
     _lib.check(rc, "host_batch")
+
+
+BATCH_MAX = 8  # ops per device launch (tf_elementwise_batch)
+
+
+def batch(calls):
+    """Run several kernels over the same planes as ONE device launch per 8 calls.
+
+    ``calls`` as for ``host_batch``.  CUDA-tensor planes: ``tf_elementwise_batch``
+    on the current stream; each distinct input plane is read from HBM once,
+    every call's output is written once, and the results equal running the calls
+    one by one (bit for bit).  Host (numpy) planes go to ``host_batch``.  No
+    output may overlap any input of the batch (ValueError before any launch).
+    """
+    import ctypes
+
+    if not calls:
+        return
+    ops, ins, outs, first, descs = _parse_batch(calls, "batch")
+    if first.kind != "cuda":
+        return host_batch(calls)
+    # every group's outputs against every input of the whole batch
+    span = first.n * first.dtype.itemsize
+    in_ptrs = [p for p in ins if p is not None]
+    for o in outs:
+        if first.n and any(o < q + span and q < o + span for q in in_ptrs):
+            raise ValueError("batch: out must not alias an input")
+    L = _lib.lib()
+    _lib.ensure_device(first.device)
+    with torch.cuda.device(first.device):
+        stream = torch.cuda.current_stream().cuda_stream
+        for g in range(0, len(ops), BATCH_MAX):
+            k = min(BATCH_MAX, len(ops) - g)
+            arr_ops = (ctypes.c_int * k)(*ops[g:g + k])
+            rc = L.tf_elementwise_batch(k, arr_ops, _dtype_id(first.dtype), first.n,
+                                        _lib.ptr_array(ins[4 * g:4 * (g + k)]),
+                                        _lib.ptr_array(outs[2 * g:2 * (g + k)]), stream)
+            _lib.check(rc, "batch")
 
 
 # --------------------------------------------------------------------------

@@ -441,3 +441,127 @@ def test_reused_pageable_planes_get_page_locked(oracle):
     del x, y, out
     gc.collect()
     assert not (addrs & set(K._REG)), "registrations outlived their arrays"
+
+
+# ---- device batch (tf_elementwise_batch): several ops in ONE launch ---------
+
+
+def _batch_call(K, name, planes, out):
+    spec = K.KERNELS[name]
+    T = K.TwofoldArray
+    if spec.arity == "22":
+        return (name, T(planes[0], planes[1]), T(planes[2], planes[3]), out)
+    if spec.arity == "21":
+        return (name, T(planes[0], planes[1]), planes[2], out)
+    if spec.arity == "11":
+        return (name, planes[0], planes[1], out)
+    if spec.arity == "u2":
+        return (name, T(planes[0], planes[1]), out)
+    return (name, planes[0], out)
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+@pytest.mark.parametrize("offset", [0, 1, "mixed"])
+def test_device_batch_all_ops_match_one_by_one(fmt, offset):
+    # every registry op in batches of 8 (plus a partial group), planes shared
+    # between ops, wide exponents and specials; aligned, commonly misaligned and
+    # mixed-misaligned (scalar path) views: bits equal to one launch per op
+    from paper_1401_6235_b200 import kernels as K
+
+    dt = torch.float64 if fmt == "f64" else torch.float32
+    npdt = np.float64 if fmt == "f64" else np.float32
+    n = 3 * 4096 + 29
+    rng = np.random.default_rng(5)
+    shared = []
+    for k in range(4):
+        v = (rng.uniform(-1, 1, n) * np.exp2(rng.integers(-30, 31, n))).astype(npdt)
+        v[:8] = np.array([0.0, -0.0, np.inf, -np.inf, np.nan, 1e-310, 3.0, -2.5], dtype=npdt)
+        shared.append(v)
+    if offset == "mixed":
+        offs = [1, 0, 3, 2]
+    else:
+        offs = [offset] * 4
+
+    def plane(k):
+        buf = torch.empty(n + offs[k], dtype=dt, device=DEV)
+        p = buf[offs[k]:]
+        p.copy_(torch.from_numpy(shared[k]))
+        return p
+
+    planes = [plane(k) for k in range(4)]
+    names = [row[0] for row in K._TABLE]
+    calls, outs, want = [], [], []
+    for i, name in enumerate(names):
+        nin = {"22": 4, "21": 3, "11": 2, "u2": 2, "u1": 1}[K.KERNELS[name].arity]
+        ps = [planes[(i + k) % 4] for k in range(nin)]
+        oo = offs[i % 4] if offset == "mixed" else offs[0]
+        o = K.TwofoldArray(*(torch.full((n + oo,), 7.0, dtype=dt, device=DEV)[oo:]
+                             for _ in range(2)))
+        calls.append(_batch_call(K, name, ps, o))
+        outs.append(o)
+        w = K.empty_twofold(n, dt, device=DEV)
+        K.KERNELS[name].func(*calls[-1][1:-1], w)
+        want.append(w)
+    K.batch(calls)
+    torch.cuda.synchronize()
+    for name, o, w in zip(names, outs, want):
+        assert bits_equal(o.value.cpu().numpy(), w.value.cpu().numpy()), name
+        assert bits_equal(o.error.cpu().numpy(), w.error.cpu().numpy()), name
+
+
+def test_device_batch_config2_step_vs_oracle(oracle):
+    # the bench's config-2 step as one launch: x, y shared by add/sub/mul; the
+    # divisor and sqrt planes of their own
+    from paper_1401_6235_b200 import kernels as K
+
+    n = (1 << 22) + 5
+    a = _config2_inputs("vtadd2", n, 91)
+    d = _config2_inputs("vtdiv2", n, 92)
+    q = _config2_inputs("vtsqrt1", n, 93)
+    t = lambda v: torch.from_numpy(v).to(DEV)  # noqa: E731
+    X, Y = K.TwofoldArray(t(a[0]), t(a[1])), K.TwofoldArray(t(a[2]), t(a[3]))
+    D = K.TwofoldArray(t(d[2]), t(d[3]))
+    Q = K.TwofoldArray(t(q[0]), t(q[1]))
+    outs = [K.empty_twofold(n, torch.float64, device=DEV) for _ in range(5)]
+    K.batch([("vtadd2", X, Y, outs[0]), ("vtsub2", X, Y, outs[1]), ("vtmul2", X, Y, outs[2]),
+             ("vtdiv2", X, D, outs[3]), ("vtsqrt1", Q, outs[4])])
+    torch.cuda.synchronize()
+    for o, (name, ins) in zip(outs, [("vtadd2", a), ("vtsub2", a), ("vtmul2", a),
+                                     ("vtdiv2", (a[0], a[1], d[2], d[3])), ("vtsqrt1", q)]):
+        w0, w1 = oracle.elementwise(name, *ins)
+        assert bits_equal(o.value.cpu().numpy(), w0), name
+        assert bits_equal(o.error.cpu().numpy(), w1), name
+
+
+def test_device_batch_contract():
+    # chains rejected before any launch (outputs untouched); n == 0 no-op; mixed
+    # dtypes rejected; host planes route to host_batch
+    from paper_1401_6235_b200 import _lib
+    from paper_1401_6235_b200 import kernels as K
+
+    n = 1000
+    x = K.TwofoldArray(torch.ones(n, dtype=torch.float64, device=DEV),
+                       torch.zeros(n, dtype=torch.float64, device=DEV))
+    o1 = K.TwofoldArray(torch.full((n,), 5.0, dtype=torch.float64, device=DEV),
+                        torch.full((n,), 5.0, dtype=torch.float64, device=DEV))
+    o2 = K.empty_twofold(n, torch.float64, device=DEV)
+    with pytest.raises(ValueError, match="alias"):
+        K.batch([("vtadd2", x, x, o1), ("vtmul2", o1, x, o2)])
+    torch.cuda.synchronize()
+    assert (o1.value == 5.0).all() and (o1.error == 5.0).all()
+    with pytest.raises(ValueError, match="mix"):
+        K.batch([("vtadd2", x, x, o1), ("vtadd2", K.TwofoldArray(x.value.float(), x.error.float()),
+                                        K.TwofoldArray(x.value.float(), x.error.float()),
+                                        K.empty_twofold(n, torch.float32, device=DEV))])
+    e = K.empty_twofold(0, torch.float64, device=DEV)
+    z = K.TwofoldArray(x.value[:0], x.error[:0])
+    K.batch([("vtadd2", z, z, e)])
+    K.batch([])
+    # the C ABI rejects more than 8 ops and unknown op ids
+    ops = (__import__("ctypes").c_int * 9)(*([0] * 9))
+    assert _lib.lib().tf_elementwise_batch(9, ops, _lib.TF_F64, 1, None, None, None) != 0
+    # host planes: routed to the pipelined host path
+    xh = K.TwofoldArray(np.ones(n), np.zeros(n))
+    oh = K.empty_twofold(n, np.float64, device="cpu")
+    K.batch([("vtadd2", xh, xh, oh)])
+    assert (oh.value == 2.0).all() and (oh.error == 0.0).all()
