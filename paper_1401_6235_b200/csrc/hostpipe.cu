@@ -120,6 +120,8 @@ struct HostPipe {
   static constexpr int MAX_SLOTS = 8;
   int slots = 3;
   int64_t chunk_bytes = 32ll << 20;  // per plane per slot (sweep: 32 MB best, r1 profiles)
+  int64_t min_chunks = 8;             // split smaller planes into this many chunks ...
+  int64_t min_chunk_bytes = 1 << 20;  // ... of at least this many bytes (sweep: r1s2_host_chunk_sweep.txt)
   std::mutex mu;
   bool ready = false;
   cudaStream_t st[MAX_SLOTS] = {};
@@ -147,6 +149,14 @@ static int pipe_init(HostPipe& p) {
     long k = atol(v);
     if (k >= 1 && k <= 1024) p.chunk_bytes = (int64_t)k << 20;
   }
+  if (const char* v = getenv("TF_HOST_MIN_CHUNKS")) {
+    long k = atol(v);
+    if (k >= 1 && k <= 64) p.min_chunks = k;
+  }
+  if (const char* v = getenv("TF_HOST_MIN_CHUNK_KB")) {
+    long k = atol(v);
+    if (k >= 4 && k <= (1 << 20)) p.min_chunk_bytes = (int64_t)k << 10;
+  }
   for (int s = 0; s < p.slots; s++) {
     cudaError_t e = cudaStreamCreateWithFlags(&p.st[s], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p.done[s], cudaEventDisableTiming);
@@ -156,12 +166,18 @@ static int pipe_init(HostPipe& p) {
   return TF_OK;
 }
 
-// Bytes per plane per slot for a call staging NP planes: the configured chunk,
-// shortened (4 KB multiples) so that NP planes x slots fit the staging budget.
-static int64_t plane_bytes(const HostPipe& p, int NP) {
+// Bytes per plane per slot for a call staging NP planes of `total` bytes each:
+// the configured chunk, shortened (4 KB multiples) so that NP planes x slots fit
+// the staging budget, and so that a plane of a few chunks still splits into
+// min_chunks (of >= min_chunk_bytes each): with one chunk, H2D, kernel and D2H run back
+// to back and the two link directions never overlap.
+static int64_t plane_bytes(const HostPipe& p, int NP, int64_t total) {
   int64_t b = STAGING_BUDGET / ((int64_t)NP * p.slots);
   if (b > p.chunk_bytes) b = p.chunk_bytes;
-  b &= ~int64_t(4095);
+  int64_t split = (total + p.min_chunks - 1) / p.min_chunks;
+  if (split < p.min_chunk_bytes) split = p.min_chunk_bytes;
+  if (b > split) b = split;
+  b = (b + 4095) & ~int64_t(4095);
   return b < 4096 ? 4096 : b;
 }
 
@@ -289,7 +305,7 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
   bool any_pageable = false;
   for (int q = 0; q < U; q++) any_pageable |= !(pin_in[q] = is_pinned(uniq[q]));
   for (int o = 0; o < 2 * nops; o++) any_pageable |= !(pin_out[o] = is_pinned(out[o]));
-  const int64_t pb = plane_bytes(p, NP);
+  const int64_t pb = plane_bytes(p, NP, n * (int64_t)tsz);
   if ((rc = ensure_arenas(p, (size_t)pb * NP, any_pageable))) return rc;
   if (any_pageable && (rc = ensure_pool(p))) return rc;
   auto dplane = [&](int s, int q) { return static_cast<char*>(p.darena[s]) + (size_t)q * pb; };
