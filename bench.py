@@ -115,6 +115,13 @@ def _fill(t, kind, seed, offset, lo, hi, head=None):
     workloads.fill(t, kind, seed, offset, lo, hi, head)
 
 
+def _pinned_empty(n, esz):
+    import torch
+
+    dt = torch.float64 if esz == 8 else torch.float32
+    return torch.empty(n, dtype=dt, pin_memory=True).numpy()
+
+
 def _pinned_copy(t):
     import torch
 
@@ -124,8 +131,8 @@ def _pinned_copy(t):
 
 
 # the e2e (host-plane) leg runs on the first E2E_MAX elements of each plane: it
-# is PCIe-bound, so a 1 GiB-per-plane sample measures the same rate while
-# keeping pinned host memory at ~10 GiB per rank (8 ranks share one host)
+# is PCIe-bound, so a 1 GiB-per-plane sample (0.5 GiB with several ranks on one
+# host) measures the same rate while bounding pinned host memory per rank
 E2E_MAX = 1 << 27
 
 
@@ -744,8 +751,12 @@ def run_elementwise(args, rank, world, local):
         barrier(world)
         dt = max_over_ranks(dt, world)
         # the same step as ONE host_batch call: each distinct host plane crosses
-        # the link once per chunk (x, y shared by add/sub/mul/div)
-        batch = [(op.name,) + op.host_args for op in ops]
+        # the link once per chunk (x, y shared by add/sub/mul/div); every op
+        # writes its own pinned output planes
+        ne_b = min(n, E2E_MAX)
+        bouts = [KM.TwofoldArray(_pinned_empty(ne_b, esz), _pinned_empty(ne_b, esz))
+                 for _ in ops]
+        batch = [(op.name,) + op.host_args[:-1] + (o,) for op, o in zip(ops, bouts)]
         KM.host_batch(batch)
         barrier(world)
         t0 = time.perf_counter()
@@ -1048,8 +1059,11 @@ def run_config5(args, rank, world, local):
 
 
 def main():
+    global E2E_MAX
     args = parse()
     rank, world, local = env_rank()
+    if world > 1:  # ranks of one node share its host memory: 0.5 GiB host planes
+        E2E_MAX = 1 << 26
     if args.impl == "reference":
         return run_reference(args, rank, world)
     import torch
