@@ -395,18 +395,23 @@ def test_cuda_graph_capture_and_replay(oracle):
     Y = K.TwofoldArray(_t(ins[2]), _t(ins[3]))
     o1, o2 = K.empty_twofold(n, torch.float64), K.empty_twofold(n, torch.float64)
     red = torch.empty(2, dtype=torch.float64, device=DEV)
+    o3, o4 = K.empty_twofold(n, torch.float64), K.empty_twofold(n, torch.float64)
     s = torch.cuda.Stream()
-    with torch.cuda.stream(s):  # warm (self-test, occupancy, workspace) outside capture
+
+    def step():
         K.vtdiv2(X, Y, o1)
         K.vtadd2(o1, Y, o2)
         R.vtdot(o2.value, Y.value, out=red)
+        K.batch([("vtdiv2", X, Y, o3), ("vtmul2", o2, Y, o4)])  # one launch
+
+    with torch.cuda.stream(s):  # warm (self-test, occupancy, workspace) outside capture
+        step()
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=s):
-        K.vtdiv2(X, Y, o1)
-        K.vtadd2(o1, Y, o2)
-        R.vtdot(o2.value, Y.value, out=red)
-    for buf in (o1.value, o1.error, o2.value, o2.error, red):
+        step()
+    for buf in (o1.value, o1.error, o2.value, o2.error, red, o3.value, o3.error,
+                o4.value, o4.error):
         buf.fill_(7.0)
     g.replay()
     g.replay()
@@ -417,6 +422,9 @@ def test_cuda_graph_capture_and_replay(oracle):
     assert bits_equal(o2.value.cpu().numpy(), w2[0]) and bits_equal(o2.error.cpu().numpy(), w2[1])
     wr = oracle.reduce("dot", w2[0], ins[2], geometry=R.geometry(np.float64))
     assert (red[0].item(), red[1].item()) == (float(wr[0]), float(wr[1]))
+    w4 = oracle.elementwise("vtmul2", w2[0], w2[1], ins[2], ins[3])
+    assert bits_equal(o3.value.cpu().numpy(), w1[0]) and bits_equal(o3.error.cpu().numpy(), w1[1])
+    assert bits_equal(o4.value.cpu().numpy(), w4[0]) and bits_equal(o4.error.cpu().numpy(), w4[1])
 
 
 def test_reused_pageable_planes_get_page_locked(oracle):

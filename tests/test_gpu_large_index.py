@@ -40,3 +40,30 @@ def test_elementwise_and_reduction_past_2g_elements(oracle):
     xh = x.cpu().numpy()
     w = oracle.reduce("sum", xh, geometry=R.geometry(np.float32))
     assert (zs.value, zs.error) == (float(w[0]), float(w[1]))
+
+
+def test_device_batch_past_2g_elements():
+    # the device batch (one launch, two ops over one shared plane) past 2^31
+    # elements: vtmul (TwoProd) and vtsqrt checked against one launch per op on
+    # a 1/1024 sample of positions spread over the whole index range
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import workloads as W
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 60e9:
+        pytest.skip("needs ~60 GB of free HBM")
+    x = W.fill(torch.empty(N, dtype=torch.float32, device="cuda"), W.LOGU_POS, 21, 0, -20.0, 20.0)
+    a = K.empty_twofold(N, torch.float32, K.CoupledArray)
+    b = K.empty_twofold(N, torch.float32, K.CoupledArray)
+    K.batch([("vtmul", x, x, a), ("vtsqrt", x, b)])
+    idx = torch.arange(0, N, 1021, device="cuda")
+    idx = torch.cat([idx, torch.tensor([N - 1], device="cuda")])
+    xs = x[idx].contiguous()
+    del x
+    torch.cuda.empty_cache()
+    wa = K.empty_twofold(xs.numel(), torch.float32, K.CoupledArray)
+    wb = K.empty_twofold(xs.numel(), torch.float32, K.CoupledArray)
+    K.vtmul(xs, xs, wa)
+    K.vtsqrt(xs, wb)
+    assert torch.equal(a.value[idx], wa.value) and torch.equal(a.error[idx], wa.error)
+    assert torch.equal(b.value[idx], wb.value) and torch.equal(b.error[idx], wb.error)
