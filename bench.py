@@ -423,6 +423,30 @@ def cpu_baseline_reduce(xh, yh, n_sample, reps=3):
     return 2 * n_sample / (t_dot + t_sum), nt
 
 
+def exact_check(xh, yh, zdot, zsum, nt):
+    """The timed run's own results at full size against the oracle's exact
+    integer-limb accumulator: achieved condition numbers and the north star's
+    bound |(z0+z1) - exact| <= 4u * sum|terms| (u = 2^-53)."""
+    from fractions import Fraction
+
+    from oracle import oracle as o
+
+    u4 = 4 * Fraction(1, 2**53)
+    out = {}
+    for name, rop, planes, z in (("vtdot", "dot", (xh, yh), zdot), ("vtsum", "sum", (xh,), zsum)):
+        s, t = o.exact(rop, *planes, nthreads=nt)
+        err = abs(Fraction(z[0]) + Fraction(z[1]) - s)
+        c = (2 if rop == "dot" else 1) * t / abs(s) if s else float("inf")
+        out[name] = {"cond": float(c), "bound_ok": bool(err <= u4 * t),
+                     "err_over_bound": float(err / (u4 * t)) if t else 0.0,
+                     "z0_rel_err": float(abs(Fraction(z[0]) - s) / abs(s)) if s else None,
+                     "z0_plus_z1_rel_err": float(err / abs(s)) if s else None}
+    out["how"] = ("oracle exact accumulator (144 32-bit limbs, exact 106-bit products) over "
+                  "all %d elements; cond(dot) = 2*sum|x*y|/|sum x*y|, cond(sum) = "
+                  "sum|x|/|sum x|" % len(xh))
+    return out
+
+
 def cpu_baseline_horner(xh, coeffs, n_sample, reps=3):
     """Oracle twofold Horner (C, OpenMP, all host threads) on a bounded sample."""
     from oracle import oracle as o
@@ -946,6 +970,8 @@ def run_config4(args, rank, world, local):
                "sample": "first %d elements of the bench's own planes, vtdot + vtsum (best of 3 "
                          "each), oracle/twofold_oracle.c canonical order, OpenMP on %d threads"
                          % (ns, nt)}
+        log("full-size check against the exact accumulator")
+        cpu["check"] = exact_check(xh, yh, part.cpu().tolist(), part2.cpu().tolist(), nt)
     if rank == 0:
         gbs = 16 * n / (dot_ms * 1e-3) / 1e9
         line = {

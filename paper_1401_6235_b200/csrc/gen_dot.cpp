@@ -11,6 +11,13 @@
 // The running dot is carried in double-double (TwoProd + TwoSum), accurate to
 // ~u^2 * sum|x_i y_i| — far below what the cancellation needs.  No final
 // permutation is applied.  Compiled with -ffp-contract=off.
+//
+// One calibration beyond the published method: the LAST pair's target (the
+// value the whole dot ends on) is +-2 * sum|x_i y_i| / cond instead of a random
+// number of unit scale.  With unit-scale final targets the achieved condition
+// number 2 sum|x_i y_i| / |sum x_i y_i| grows with n (sum|x_i y_i| ~ n 2^b /
+// log2 cond): 2.5e24 at n = 2^30 for a 1e16 target.  Calibrated, it is the
+// requested cond at every n (up to ~1/u^2, the double-double limit).
 #include <cmath>
 #include <cstdint>
 #include <thread>
@@ -30,6 +37,7 @@ inline double u01(uint64_t key, uint64_t i) { return (double)(mix(key ^ i) >> 11
 
 struct DD {
   double s = 0, c = 0;
+  double abs_sum = 0;  // sum |x_i y_i| (plain double; only scales the final target)
   void add(double p) {
     double t = s + p;
     double bv = t - s;
@@ -43,6 +51,7 @@ struct DD {
     double e = std::fma(x, y, -p);
     add(p);
     c += e;
+    abs_sum += std::fabs(p);
   }
 };
 
@@ -80,6 +89,7 @@ extern "C" int tf_gen_dot_host(int64_t n, double cond, uint64_t seed, double* x,
   for (auto& p : part) {
     run.add(p.s);
     run.c += p.c;
+    run.abs_sum += p.abs_sum;
   }
   // second half: sequential cancellation
   const int64_t m = n - n2;
@@ -90,7 +100,9 @@ extern "C" int tf_gen_dot_host(int64_t n, double cond, uint64_t seed, double* x,
     const double sc = std::ldexp(1.0, (int)e);
     double xi = (2 * u01(key, 4 * (uint64_t)i + 1) - 1) * sc;
     if (xi == 0) xi = sc;
-    const double target = (2 * u01(key, 4 * (uint64_t)i + 2) - 1) * sc;
+    double target = (2 * u01(key, 4 * (uint64_t)i + 2) - 1) * sc;
+    if (j == m - 1)  // the dot ends on this value: calibrated to the requested cond
+      target = (target < 0 ? -2.0 : 2.0) * run.abs_sum / cond;
     const double cur = run.s + run.c;
     x[i] = xi;
     y[i] = (target - cur) / xi;

@@ -52,7 +52,7 @@ def test_gen_dot_host_is_deterministic(oracle):
     assert np.array_equal(xs[0][0], xs[1][0]) and np.array_equal(xs[0][1], xs[1][1])
     s, t = oracle.exact("dot", *xs[0])
     cond = float(2 * t / abs(s))
-    assert 1e13 < cond < 1e19, cond
+    assert 0.5e16 < cond < 2e16, cond  # calibrated: the requested condition number
 
 
 def test_registry_contents():

@@ -81,7 +81,7 @@ def test_config4_full_size_dot_and_sum(oracle):
     ok, err, s, t = oracle.bound_ok(z.value, z.error, "dot", x, y)
     assert ok, (float(err), float(t))
     cond = float(2 * t / abs(s))
-    assert cond > 1e12, cond  # genuinely ill-conditioned at full size
+    assert 0.5e16 < cond < 2e16, cond  # BASELINE's cond ~1e16, at full size
     # plain double dot in the same order is far off; the twofold is not
     rel_plain = abs(float(z.value) - float(s)) / abs(float(s))
     rel_tf = float(err / abs(s))
