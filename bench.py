@@ -1040,6 +1040,23 @@ def run_config5(args, rank, world, local):
     instr = 220.0 * n
     achieved = instr / (per_ms * 1e-3)
     value = world * n * K / (elapsed_ms * 1e-3)
+    # full-size property check of the timed run's own outputs, on the device:
+    # (x-1)^20 evaluated stably (x-1 is exact for x in [0.5, 2], then 20 ulps at
+    # most) against the expanded-polynomial Horner; z1 must flag the cancellation
+    with torch.no_grad():
+        p = (x - 1.0).pow(20)
+        z0, z1 = out.value, out.error
+        nz = (z0 != 0) & (p != 0)
+        flagged = ((z1.abs() >= 0.5 * z0.abs()) & nz).sum().item()
+        rel0 = ((z0 - p).abs() / p.abs())[nz]
+        rel01 = (((z0 + z1) - p).abs() / p.abs())[nz]
+        check = {"points": n, "nonzero": int(nz.sum().item()),
+                 "flag_rate": flagged / max(1, int(nz.sum().item())),
+                 "median_rel_err_z0": rel0.median().item(),
+                 "median_rel_err_z0_plus_z1": rel01.median().item(),
+                 "how": "on the device: reference (x-1)^20 by torch.pow of the exact x-1; "
+                        "flag = |z1| >= 0.5|z0| where z0 != 0"}
+        del p, nz, rel0, rel01
     # e2e: the public API on pinned numpy planes (tf_horner_host pipeline)
     ne = min(n, E2E_MAX)
     xh = torch.empty(ne, dtype=torch.float64, pin_memory=True)
@@ -1077,6 +1094,7 @@ def run_config5(args, rank, world, local):
                     "elems_per_step": ne,
                     "path": "reduce.vthorner on pinned numpy planes -> tf_horner_host"},
             "cpu_baseline": cpu,
+            "check": check,
             "gpu_launches": world * K,
             "clocks": clk.summary(),
         }
