@@ -205,6 +205,47 @@ def _call(K, name, planes, out):
     return (name, planes[0], out)
 
 
+def ieee_check(ops, outs):
+    """Full-size properties of the timed step's own outputs, on the device with
+    plain torch ops (one IEEE-RN kernel per op, so no contraction): z0 is bitwise
+    the standard IEEE result of the heads for every op (north star); for the
+    add/sub ops z1 is bitwise the TwoSum/TwoDiff error plus the tails."""
+    import torch
+
+    res = {}
+    with torch.no_grad():
+        for op, o in zip(ops, outs):
+            P = op.planes
+            x0 = P[0]
+            y0 = P[2] if len(P) == 4 else None
+            ieee = {"vtadd2": lambda: x0 + y0, "vtsub2": lambda: x0 - y0,
+                    "vtmul2": lambda: x0 * y0, "vtdiv2": lambda: x0 / y0,
+                    "vtsqrt1": lambda: torch.sqrt(x0)}.get(op.name)
+            if ieee is None:
+                continue
+            r = {"z0_is_ieee": bool(torch.equal(o.value, ieee()))}
+            if op.name in ("vtadd2", "vtsub2"):
+                x1, y1 = P[1], P[3]
+                if op.name == "vtadd2":
+                    s_ = x0 + y0
+                    bv = s_ - x0
+                    av = s_ - bv
+                    e = (x0 - av) + (y0 - bv)
+                    z1 = (x1 + y1) + e
+                else:
+                    s_ = x0 - y0
+                    bv = x0 - s_
+                    av = s_ + bv
+                    e = (x0 - av) + (bv - y0)
+                    z1 = (x1 - y1) + e
+                r["z1_is_twosum_identity"] = bool(torch.equal(o.error, z1))
+                del s_, bv, av, e, z1
+            res[op.name] = r
+    res["how"] = ("all elements, on the device: torch ops, one IEEE-RN kernel each "
+                  "(arith.py:61-64, 74-77 for the error planes)")
+    return res
+
+
 def device_batch_leg(args, ops, n, esz, peak, world):
     """The step's ops as ONE launch (kernels.batch -> tf_elementwise_batch), each
     op into its own output planes; each distinct input plane is read from HBM
@@ -237,13 +278,14 @@ def device_batch_leg(args, ops, n, esz, peak, world):
         ev[s][1].record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev), world) / args.steps
+    check = ieee_check(ops, outs)
     del outs, calls
     gbs = nbytes / (ms * 1e-3) / 1e9
     return {"value": world * len(ops) * n / (ms * 1e-3), "unit": "elem-ops/s",
             "ms_per_step": ms, "bytes_per_step": nbytes, "distinct_input_planes": len(distinct),
             "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s",
                          "frac": gbs / peak},
-            "launches_per_step": 1,
+            "launches_per_step": 1, "check": check,
             "path": "kernels.batch([%d calls]) -> tf_elementwise_batch: one launch per step, "
                     "each op into its own output planes" % len(ops)}
 
