@@ -35,7 +35,17 @@ res["submul"] = {"fused_ms": ms_f, "fused_gbs": 64 * n / ms_f / 1e6}
 q = tuple(K.empty_twofold(n, torch.float64) for _ in range(3))
 cq = K.TwofoldArray(torch.abs(y0) * 1e-3, y1 * 1e-3)
 ms = timeit(lambda: F.vtquadratic(a, X, cq, q))
-res["quadratic"] = {"ms": ms, "G_inst_s": n / ms / 1e6, "gbs": 96 * n / ms / 1e6}
+res["quadratic"] = {"ms": ms, "G_inst_s": n / ms / 1e6, "gbs": 96 * n / ms / 1e6,
+                    "inputs": "c = |y|*1e-3: about half the discriminants negative (NaN roots)"}
+# real roots everywhere: c = b^2 / (4a) * U[0.1, 0.9] (disc > 0), tails at 2^-53 scale
+g = torch.Generator(device="cuda").manual_seed(7)
+u = torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 0.8 + 0.1
+c0 = x0 * x0 / (4 * a.value) * u
+c1 = c0 * 2.0**-53 * (torch.rand(n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1)
+cr = K.TwofoldArray(c0, c1)
+ms = timeit(lambda: F.vtquadratic(a, X, cr, q))
+res["quadratic_real_roots"] = {"ms": ms, "G_inst_s": n / ms / 1e6, "gbs": 96 * n / ms / 1e6,
+                               "inputs": "c = b^2/(4a) * U[0.1, 0.9]: every discriminant positive"}
 m = 1 << 24
 Av = torch.rand((3, 3, m), dtype=torch.float64, device="cuda") + 4 * torch.eye(3, dtype=torch.float64, device="cuda")[:, :, None]
 Ae = torch.zeros_like(Av)
