@@ -28,6 +28,7 @@ namespace tf {
 int ew_num_inputs(int op);
 int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* out,
               cudaStream_t stream);
+constexpr int TF_BATCH_MAX_OPS = 8;  // tf_elementwise_batch's limit
 
 // ---- a small persistent thread pool for parallel host memcpy ------------------
 class CopyPool {
@@ -122,6 +123,7 @@ struct HostPipe {
   int64_t chunk_bytes = 32ll << 20;  // per plane per slot (sweep: 32 MB best, r1 profiles)
   int64_t min_chunks = 8;             // split smaller planes into this many chunks ...
   int64_t min_chunk_bytes = 1 << 20;  // ... of at least this many bytes (sweep: r1s2_host_chunk_sweep.txt)
+  int64_t zerocopy_bytes = 16ll << 20;  // pinned planes up to this size: zero-copy kernel
   std::mutex mu;
   bool ready = false;
   cudaStream_t st[MAX_SLOTS] = {};
@@ -148,6 +150,10 @@ static int pipe_init(HostPipe& p) {
   if (const char* v = getenv("TF_HOST_CHUNK_MB")) {
     long k = atol(v);
     if (k >= 1 && k <= 1024) p.chunk_bytes = (int64_t)k << 20;
+  }
+  if (const char* v = getenv("TF_HOST_ZEROCOPY_MB")) {
+    long k = atol(v);
+    if (k >= 0 && k <= 4096) p.zerocopy_bytes = (int64_t)k << 20;
   }
   if (const char* v = getenv("TF_HOST_MIN_CHUNKS")) {
     long k = atol(v);
@@ -305,6 +311,37 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
   bool any_pageable = false;
   for (int q = 0; q < U; q++) any_pageable |= !(pin_in[q] = is_pinned(uniq[q]));
   for (int o = 0; o < 2 * nops; o++) any_pageable |= !(pin_out[o] = is_pinned(out[o]));
+  // Small calls over pinned planes: zero-copy.  ONE batch kernel reads and writes
+  // the host planes in place over PCIe (UVA-mapped), with no staging copies and
+  // no chunk pipeline; below ~16 MB per plane this beats the copy engines'
+  // fill/drain (profiles/r1s2_zerocopy.json).  Large calls keep the pipeline.
+  if (!launch && !any_pageable && nops <= TF_BATCH_MAX_OPS &&
+      n * (int64_t)tsz <= p.zerocopy_bytes) {
+    std::vector<const void*> zin((size_t)nops * 4, nullptr);
+    std::vector<void*> zout((size_t)nops * 2, nullptr);
+    bool mapped = true;
+    auto dev_ptr = [&](const void* h) -> void* {
+      void* d = nullptr;
+      if (cudaHostGetDevicePointer(&d, const_cast<void*>(h), 0) != cudaSuccess) {
+        cudaGetLastError();
+        mapped = false;
+      }
+      return d;
+    };
+    for (int o = 0; o < nops && mapped; o++) {
+      for (int k = 0; k < 4; k++)
+        if (idx[4 * o + k] >= 0) zin[4 * o + k] = dev_ptr(in[4 * o + k]);
+      for (int k = 0; k < 2; k++) zout[2 * o + k] = dev_ptr(out[2 * o + k]);
+    }
+    if (mapped) {
+      rc = tf_elementwise_batch(nops, ops, dtype, n, zin.data(), zout.data(), p.st[0]);
+      if (rc) return rc;
+      cudaError_t e = cudaStreamSynchronize(p.st[0]);
+      if (e != cudaSuccess) return cuda_status(e, who);
+      guard.ok = true;
+      return TF_OK;
+    }
+  }
   const int64_t pb = plane_bytes(p, NP, n * (int64_t)tsz);
   if ((rc = ensure_arenas(p, (size_t)pb * NP, any_pageable))) return rc;
   if (any_pageable && (rc = ensure_pool(p))) return rc;

@@ -65,6 +65,22 @@ for dt in (np.float64, np.float32):
     if not (np.array_equal(out.value, w[0]) and np.array_equal(out.error, w[1])):
         bad += 1
         print("host path mismatch", dt)
+# pinned host planes (small: the zero-copy kernel by default; TF_HOST_ZEROCOPY_MB
+# selects the staged pipeline or forces zero-copy), unaligned interior views
+for dt in (np.float64, np.float32):
+    n = 3 * (1 << 16) + 7
+    tdt = torch.float64 if dt == np.float64 else torch.float32
+    pins = [torch.from_numpy(rng.uniform(0.5, 2, n + 3).astype(dt)).pin_memory().numpy()[k % 3:k % 3 + n]
+            for k in range(4)]
+    outs = [torch.empty(n + 1, dtype=tdt).pin_memory().numpy()[1:] for _ in range(4)]
+    X, Y = K.TwofoldArray(pins[0], pins[1]), K.TwofoldArray(pins[2], pins[3])
+    K.host_batch([("vtdiv2", X, Y, K.TwofoldArray(outs[0], outs[1])),
+                  ("vtadd2", X, Y, K.TwofoldArray(outs[2], outs[3]))])
+    for name, a, b in (("vtdiv2", outs[0], outs[1]), ("vtadd2", outs[2], outs[3])):
+        w = o.elementwise(name, *pins)
+        if not (np.array_equal(a, w[0]) and np.array_equal(b, w[1])):
+            bad += 1
+            print("pinned host path mismatch", name, dt)
 torch.cuda.synchronize()
 print("sanitize smoke done, mismatches:", bad)
 sys.exit(1 if bad else 0)
