@@ -43,3 +43,23 @@ def test_reference_arm_non_zero_ranks_exit_quietly():
                         "--steps", "1", "--warmup", "1"], capture_output=True, text=True,
                        timeout=120, cwd=ROOT, env=e)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_exact_check_of_a_generated_dot(oracle):
+    # the config-4 full-size check on a small instance: the calibrated generator
+    # hits the requested condition and the canonical-order twofold is in bound
+    import numpy as np
+
+    sys.path.insert(0, str(ROOT))
+    import bench
+    from paper_1401_6235_b200 import _lib
+
+    n = 1 << 15
+    x, y = np.empty(n), np.empty(n)
+    assert _lib.lib().tf_gen_dot_host(n, 1e16, 4242, x.ctypes.data, y.ctypes.data) == 0
+    zd = oracle.reduce("dot", x, y, geometry=(2, 256, 128))
+    zs = oracle.reduce("sum", x, geometry=(2, 256, 128))
+    c = bench.exact_check(x, y, [float(zd[0]), float(zd[1])], [float(zs[0]), float(zs[1])], 2)
+    assert c["vtdot"]["bound_ok"] and c["vtsum"]["bound_ok"]
+    assert 0.5e16 < c["vtdot"]["cond"] < 2e16
+    assert c["vtdot"]["z0_plus_z1_rel_err"] < 1e-10 < c["vtdot"]["z0_rel_err"]
