@@ -247,6 +247,14 @@ static int begin_exchange(XCtx& c, const int64_t* counts, int mode, const char* 
   return TF_OK;
 }
 
+// Launch status of an exchange; a publish that never reached the device leaves
+// nothing pending to collect.
+static int end_exchange(XCtx& c, int mode, const char* who) {
+  const int rc = launch_status(who);
+  if (rc && mode == XM_PUBLISH) c.pending = false;
+  return rc;
+}
+
 static int xgpu_combine_impl(int dtype, void* out, const int64_t* counts, void* stream, int mode,
                              const char* who) {
   XCtx* c = ctx_for_current(nullptr);
@@ -259,7 +267,7 @@ static int xgpu_combine_impl(int dtype, void* out, const int64_t* counts, void* 
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dtype == TF_F64) launch_exchange<double>(out, x, c->status, mode, s);
   else launch_exchange<float>(out, x, c->status, mode, s);
-  return launch_status(who);
+  return end_exchange(*c, mode, who);
 }
 
 static int xgpu_reduce_impl(int rop, int dtype, int64_t n, const void* a, const void* b,
@@ -284,10 +292,13 @@ static int xgpu_reduce_impl(int rop, int dtype, int64_t n, const void* a, const 
   const size_t tsz = dtype == TF_F64 ? 8 : 4;
   if (n == 0) {  // nothing to reduce: (+0, +0), skipped by the fold (count 0)
     cudaError_t e = cudaMemsetAsync(out, 0, 2 * tsz, s);
-    if (e != cudaSuccess) return cuda_status(e, who);
+    if (e != cudaSuccess) {
+      if (mode == XM_PUBLISH) c->pending = false;
+      return cuda_status(e, who);
+    }
     if (dtype == TF_F64) launch_exchange<double>(out, x, c->status, mode, s);
     else launch_exchange<float>(out, x, c->status, mode, s);
-    return launch_status(who);
+    return end_exchange(*c, mode, who);
   }
 #define XR(ROP)                                                                                   \
   case ROP:                                                                                       \
@@ -296,7 +307,7 @@ static int xgpu_reduce_impl(int rop, int dtype, int64_t n, const void* a, const 
     break;
   switch (rop) { XR(TF_RSUM) XR(TF_RSUM2) XR(TF_RDOT) }
 #undef XR
-  return launch_status(who);
+  return end_exchange(*c, mode, who);
 }
 }  // namespace tf
 
