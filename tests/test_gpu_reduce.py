@@ -231,6 +231,50 @@ def test_horner_generic_degree_vs_oracle(oracle):
     assert np.array_equal(out.error.cpu().numpy().view(np.uint64), w1.view(np.uint64))
 
 
+def _bits_eq_nan(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    na, nb = np.isnan(a), np.isnan(b)
+    u = np.uint64 if a.dtype == np.float64 else np.uint32
+    return np.array_equal(na, nb) and np.array_equal(a[~na].view(u), b[~nb].view(u))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+@pytest.mark.parametrize("deg", [20, 7])
+def test_horner_specials_bit_exact(oracle, dt, deg):
+    # Horner through every IEEE corner: zero and -0 operands, infinities, NaN,
+    # overflow to inf (and TwoSum intermediates overflowing in the top binade
+    # while the sum stays finite), subnormals, and steps whose error is exactly 0
+    from paper_1401_6235_b200 import kernels as K
+    from paper_1401_6235_b200 import reduce as R
+
+    rng = np.random.default_rng(deg)
+    big = np.finfo(dt).max
+    tiny = np.finfo(dt).smallest_subnormal
+    xs = np.array([0.0, -0.0, 1.0, -1.0, 2.0, 0.5, np.inf, -np.inf, np.nan, big, -big, tiny,
+                   -tiny, 1e-30, 3.0, 1.0 + 2**-20], dtype=dt)
+    coeff_sets = [
+        R.binomial_coeffs(deg),
+        [0.0] * (deg + 1),
+        [-0.0] * (deg + 1),
+        [(-0.0 if k % 2 else 0.0) for k in range(deg + 1)],
+        [(1.0 if k % 3 == 0 else -0.0) for k in range(deg + 1)],
+        [float(big)] * (deg + 1),
+        [float(tiny) * (k + 1) for k in range(deg + 1)],
+        [np.inf] + [1.0] * deg,
+        [1.0] * deg + [np.nan],
+        list(rng.integers(-3, 4, deg + 1).astype(float)),
+    ]
+    x = np.concatenate([xs, rng.uniform(-3, 3, 4096).astype(dt),
+                        rng.integers(-2, 3, 1024).astype(dt)])
+    for c in coeff_sets:
+        c = [float(v) for v in np.asarray(c, dtype=dt)]
+        out = K.empty_twofold(x.shape[0], torch.float64 if dt == np.float64 else torch.float32)
+        R.vthorner(c, _t(x), out)
+        w0, w1 = oracle.horner(c, x)
+        assert _bits_eq_nan(out.value.cpu().numpy(), w0), c[:3]
+        assert _bits_eq_nan(out.error.cpu().numpy(), w1), c[:3]
+
+
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("pin", [False, True])
 @pytest.mark.parametrize("rop", ["sum", "sum2", "dot"])

@@ -50,7 +50,13 @@ for dt in (np.float64, np.float32):
                 print("reduce mismatch", rop, dt, n)
     xs = rng.uniform(0.9, 1.1, 999).astype(dt)
     out = K.empty_twofold(999, torch.float64 if dt == np.float64 else torch.float32)
-    R.vthorner(R.binomial_coeffs(20), put(xs), out)
+    for cf in (R.binomial_coeffs(20), [0.5, -0.0, 3.0, -0.0, 1.0, -2.0, 0.0]):
+        R.vthorner(cf, put(xs), out)
+        w = o.horner(cf, xs)
+        if not (np.array_equal(out.value.cpu().numpy(), w[0]) and
+                np.array_equal(out.error.cpu().numpy(), w[1])):
+            bad += 1
+            print("horner mismatch", dt, len(cf))
     p = IL.from_split(K.TwofoldArray(put(xs), put(xs)))
     po = torch.empty_like(p)
     IL.vtadd2(p, p, po)
