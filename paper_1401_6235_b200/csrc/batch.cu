@@ -218,6 +218,15 @@ extern "C" int tf_elementwise_batch(int nops, const int* ops, int dtype, int64_t
     for (int k = 0; k < nin; k++)
       if (!in[4 * o + k]) return fail(TF_EINVAL, std::string(who) + ": null plane");
   }
+  // outputs either coincide (later ops overwrite, as run one by one) or are
+  // disjoint: a partial overlap has no per-element order that matches
+  for (int w = 0; w < 2 * nops; w++)
+    for (int v = w + 1; v < 2 * nops; v++) {
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(out[w]);
+      const uintptr_t b0 = reinterpret_cast<uintptr_t>(out[v]);
+      if (a0 != b0 && a0 < b0 + span && b0 < a0 + span)
+        return fail(TF_EINVAL, std::string(who) + ": out planes overlap each other");
+    }
   // no op may read what any op of the batch writes (no intra-batch chains)
   for (int w = 0; w < 2 * nops; w++) {
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(out[w]);

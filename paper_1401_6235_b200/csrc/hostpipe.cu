@@ -283,8 +283,17 @@ static int host_batch(int nops, const int* ops, int dtype, int64_t n, const void
       idx[4 * o + k] = u;
     }
   }
-  // no op may read what another op of the batch writes (no intra-batch chains)
+  // outputs either coincide (later ops overwrite, as run one by one) or are
+  // disjoint: a partial overlap has no chunk order that matches
   const uintptr_t span = (uintptr_t)n * tsz;
+  for (int w = 0; w < 2 * nops && n; w++)
+    for (int v = w + 1; v < 2 * nops; v++) {
+      const uintptr_t a0 = reinterpret_cast<uintptr_t>(out[w]);
+      const uintptr_t b0 = reinterpret_cast<uintptr_t>(out[v]);
+      if (a0 != b0 && a0 < b0 + span && b0 < a0 + span)
+        return fail(TF_EINVAL, std::string(who) + ": out planes overlap each other");
+    }
+  // no op may read what another op of the batch writes (no intra-batch chains)
   for (int o = 0; o < 2 * nops; o++) {
     const uintptr_t a0 = reinterpret_cast<uintptr_t>(out[o]);
     for (const void* u : uniq) {

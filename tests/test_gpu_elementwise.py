@@ -561,6 +561,22 @@ def test_device_batch_contract():
         K.batch([("vtadd2", x, x, o1), ("vtadd2", K.TwofoldArray(x.value.float(), x.error.float()),
                                         K.TwofoldArray(x.value.float(), x.error.float()),
                                         K.empty_twofold(n, torch.float32, device=DEV))])
+    # outputs of different calls: identical planes are fine (later calls win, as
+    # one by one); partially overlapping ones are rejected before any launch
+    buf = torch.zeros(2 * n + 8, dtype=torch.float64, device=DEV)
+    oa = K.TwofoldArray(buf[:n], buf[n + 8:])
+    ob = K.TwofoldArray(buf[3:n + 3], torch.empty(n, dtype=torch.float64, device=DEV))
+    with pytest.raises(ValueError, match="overlap"):
+        K.batch([("vtadd2", x, x, oa), ("vtmul2", x, x, ob)])
+    K.batch([("vtadd2", x, x, o2), ("vtmul2", x, x, o2)])  # same planes: vtmul2 wins
+    w = K.empty_twofold(n, torch.float64, device=DEV)
+    K.vtmul2(x, x, w)
+    assert torch.equal(o2.value, w.value) and torch.equal(o2.error, w.error)
+    hb = np.zeros(2 * n + 8)
+    with pytest.raises(ValueError, match="overlap"):
+        xh2 = K.TwofoldArray(np.ones(n), np.zeros(n))
+        K.host_batch([("vtadd2", xh2, xh2, K.TwofoldArray(hb[:n], hb[n + 8:])),
+                      ("vtmul2", xh2, xh2, K.TwofoldArray(hb[3:n + 3], np.empty(n)))])
     e = K.empty_twofold(0, torch.float64, device=DEV)
     z = K.TwofoldArray(x.value[:0], x.error[:0])
     K.batch([("vtadd2", z, z, e)])
