@@ -181,3 +181,25 @@ def test_empty_twofold_host_and_errors():
     assert type(z) is K.CoupledArray and z.error.dtype == np.float32
     with pytest.raises(ValueError, match="float32 or float64"):
         K.empty_twofold(5, np.int32)
+
+
+def test_batch_validation_before_any_launch():
+    # kernels.batch / host_batch validate every call (the reference's _check
+    # messages) and the batch as a whole before the library is touched
+    from paper_1401_6235_b200 import kernels as K
+
+    n = 16
+    x = K.TwofoldArray(np.ones(n), np.zeros(n))
+    x32 = K.TwofoldArray(np.ones(n, np.float32), np.zeros(n, np.float32))
+    o = K.empty_twofold(n, np.float64, device="cpu")
+    o32 = K.empty_twofold(n, np.float32, device="cpu")
+    K.batch([])
+    K.host_batch([])
+    with pytest.raises(ValueError, match="mix"):
+        K.batch([("vtadd2", x, x, o), ("vtadd2", x32, x32, o32)])
+    with pytest.raises(ValueError, match="vtmul2: .*alias"):
+        K.host_batch([("vtmul2", x, x, x)])
+    with pytest.raises(ValueError, match="lengths differ"):
+        K.batch([("vtadd2", x, K.TwofoldArray(np.ones(n + 1), np.zeros(n + 1)), o)])
+    with pytest.raises(KeyError):
+        K.batch([("vtnope", x, x, o)])
