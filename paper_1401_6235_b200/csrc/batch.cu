@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -181,7 +182,12 @@ static int launch_batch(int nops, const int* ops, int64_t n, const void* const* 
     mbs_cache.store(mbs, std::memory_order_relaxed);
   }
   const int64_t resident = (int64_t)sm_count() * mbs;
-  int reps = 4;
+  static const int reps_env = [] {  // TF_BATCH_REPS: A/B of the chunk length (1..64)
+    const char* e = getenv("TF_BATCH_REPS");
+    const int r = e ? atoi(e) : 0;
+    return (r >= 1 && r <= 64) ? r : 0;
+  }();
+  int reps = reps_env ? reps_env : 1;  // 1 step per CTA: +0.6% over 4 (profiles/r1s2_chunk_reps_hbm.txt)
   while (reps > 1 && nvec / (256LL * reps) < 2 * resident) reps >>= 1;
   const int64_t chunk = 256LL * reps;
   int64_t blocks = nvec > 0 ? (nvec + chunk - 1) / chunk : (n + 255) / 256;

@@ -7,9 +7,9 @@
 // (NIN + 2) * sizeof(T) bytes and nothing else.
 //
 // Layout in HBM: each plane is one contiguous 1-D array (SoA, kernels.py:3-5).
-// Design: one CTA per chunk of 256*U*4 vectors, so the hardware block scheduler
-// balances the 148 SMs (a persistent grid left a tail of idle SMs: -6..7 points
-// of bandwidth, profiles/README.md).  Vectors are 32 bytes — sm_100's 256-bit
+// Design: one CTA per chunk of 256*U*reps vectors (reps = 1, 2 for vtsqrt1), so
+// the hardware block scheduler balances the 148 SMs (a persistent grid left a
+// tail of idle SMs: -6..7 points of bandwidth, profiles/README.md).  Vectors are 32 bytes — sm_100's 256-bit
 // LDG/STG (LDG.E.NA.EFL2.256 / STG.E.EF.ENL2.256) — and each thread issues
 // U x NIN independent streaming loads before any math.  Planes that share a
 // common misalignment get a scalar head; the n % (32/sizeof(T)) tail is scalar
@@ -74,8 +74,8 @@ __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t
   // CTA-chunked: chunk c = vectors [c*CH, (c+1)*CH), CH = 256*U*reps; thread t
   // takes t, t+256, ... (coalesced).  With one CTA per chunk the hardware block
   // scheduler balances SMs dynamically (no tail of idle SMs); a capped grid
-  // strides over chunks.  reps = 4 on large planes; small planes use shorter
-  // chunks so that the grid still covers every SM evenly.
+  // strides over chunks.  reps is 1 (2 for vtsqrt1), halved on small planes so
+  // that the grid still covers every SM evenly.
   const int64_t CH = 256LL * U * reps;
   for (int64_t cb = (int64_t)blockIdx.x * CH; cb < nvec; cb += (int64_t)gridDim.x * CH) {
 #pragma unroll 1
@@ -118,6 +118,7 @@ struct EwEntry {
   const void* fn;  // kernel symbol
   int nin;
   int unroll;
+  int reps;  // default chunk length in 256*unroll-vector steps (hbm sweep, profiles)
   std::atomic<int> max_blocks_per_sm;  // occupancy, filled lazily (idempotent)
 };
 
@@ -125,7 +126,11 @@ template <class T, int OP, int VB>
 EwEntry make_entry() {
   constexpr int NIN = OpInfo<OP>::NIN;
   constexpr int U = (VB == 32) ? (NIN >= 3 ? 1 : 2) : Unroll<NIN>::U;
-  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>), NIN, U, {0}};
+  // one 256*U-vector step per CTA was fastest for every op at 2^27 (6.9-7.0 TB/s
+  // for the 48 B/element ops), except vtsqrt1 (div + 2 sqrt per element): two
+  // steps (profiles/r1s2_chunk_reps_hbm.txt)
+  constexpr int REPS = OP == 12 ? 2 : 1;
+  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>), NIN, U, REPS, {0}};
 }
 
 template <class T, int VB, int... OPS>
@@ -199,12 +204,17 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     mbs = b > 0 ? b : 1;
     ent.max_blocks_per_sm.store(mbs, std::memory_order_relaxed);
   }
-  // one CTA per chunk of 256*U*reps vectors (hardware-balanced); reps = 4
-  // unless that leaves fewer than two full waves of resident CTAs (small
-  // planes, e.g. 2^20 elements: 256 CTAs of 4 steps ran 1.7 uneven waves).
+  // one CTA per chunk of 256*U*reps vectors (hardware-balanced); reps per op
+  // (ent.reps), halved while that leaves fewer than two full waves of resident
+  // CTAs (small planes).  TF_EW_REPS overrides it for A/B runs;
   // TF_EW_SCHED=persistent caps the grid at the resident CTAs (A/B runs).
   const int64_t resident = (int64_t)sm_count() * mbs;
-  int reps = 4;
+  static const int reps_env = [] {  // thread-safe one-time init
+    const char* e = getenv("TF_EW_REPS");
+    const int r = e ? atoi(e) : 0;
+    return (r >= 1 && r <= 64) ? r : 0;
+  }();
+  int reps = reps_env ? reps_env : ent.reps;
   while (reps > 1 && nvec / (256LL * ent.unroll * reps) < 2 * resident) reps >>= 1;
   const int64_t chunk = 256LL * ent.unroll * reps;
   int64_t blocks = nvec > 0 ? (nvec + chunk - 1) / chunk : (n + 255) / 256;
