@@ -1038,7 +1038,9 @@ def run_config4(args, rank, world, local):
                                  "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 32}},
             "cpu_baseline": cpu,
             "gpu_launches": world * K * (2 + (2 if world > 1 and tp is None else 0)),
-            "reduce_transport": args.reduce_transport if world > 1 else "none (1 GPU)",
+            "reduce_transport": (args.reduce_transport if world > 1 else
+                                 "p2p (fused reduce + mailbox exchange, 1 rank)" if tp is not None
+                                 else "none (1 GPU)"),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
