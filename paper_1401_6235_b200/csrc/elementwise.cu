@@ -254,39 +254,41 @@ __global__ void __launch_bounds__(256) dotted_kernel(const T* __restrict__ x,
   }
 }
 
+// The dotted baselines get the same memory design as the twofold kernels (32-byte
+// vectors, one CTA per chunk of 256*U vectors), so the ratio column compares like
+// with like.
 template <class T, int BASE>
-__global__ void __launch_bounds__(256) dotted_vec_kernel(const typename Vec16<T>::type* __restrict__ x,
-                                                         const typename Vec16<T>::type* __restrict__ y,
-                                                         typename Vec16<T>::type* __restrict__ r,
-                                                         int64_t nvec) {
-  using V = typename Vec16<T>::type;
-  constexpr int E = Vec16<T>::N;
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = gtid; base < nvec; base += 4 * gstride) {
-    V a[4], b[4];
+__global__ void __launch_bounds__(256) dotted_vec_kernel(const Vec32<T>* __restrict__ x,
+                                                         const Vec32<T>* __restrict__ y,
+                                                         Vec32<T>* __restrict__ r, int64_t nvec) {
+  constexpr int E = Vec32<T>::N;
+  constexpr int U = 2;
+  const int64_t CH = 256LL * U;
+  for (int64_t cb = (int64_t)blockIdx.x * CH; cb < nvec; cb += (int64_t)gridDim.x * CH) {
+    Vec32<T> a[U], b[U];
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      int64_t j = base + u * gstride;
+    for (int u = 0; u < U; u++) {
+      const int64_t j = cb + u * 256 + threadIdx.x;
       if (j < nvec) {
         a[u] = ld_stream(x + j);
         if constexpr (BASE <= 2) b[u] = ld_stream(y + j);
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; u++) {
-      int64_t j = base + u * gstride;
+    for (int u = 0; u < U; u++) {
+      const int64_t j = cb + u * 256 + threadIdx.x;
       if (j < nvec) {
-        V o;
+        Vec32<T> o;
 #pragma unroll
         for (int e = 0; e < E; e++) {
-          T s = lane<T>(a[u], e), v;
-          if constexpr (BASE == 0) v = add(s, lane<T>(b[u], e));
-          else if constexpr (BASE == 1) v = mul(s, lane<T>(b[u], e));
-          else if constexpr (BASE == 2) v = dvd(s, lane<T>(b[u], e));
+          const T s = a[u].v[e];
+          T v;
+          if constexpr (BASE == 0) v = add(s, b[u].v[e]);
+          else if constexpr (BASE == 1) v = mul(s, b[u].v[e]);
+          else if constexpr (BASE == 2) v = dvd(s, b[u].v[e]);
           else if constexpr (BASE == 3) v = sqr(s);
           else v = s;
-          set_lane<T>(o, e, v);
+          o.v[e] = v;
         }
         st_stream(r + j, o);
       }
@@ -296,17 +298,16 @@ __global__ void __launch_bounds__(256) dotted_vec_kernel(const typename Vec16<T>
 
 template <class T, int BASE>
 static int dotted_t(int64_t n, const void* x, const void* y, void* r, cudaStream_t s) {
-  constexpr int E = Vec16<T>::N;
+  constexpr int E = Vec32<T>::N;
   const int64_t cap = 0x7fffffffLL;  // one CTA per chunk: hardware-balanced
-  const bool vec = aligned16(x) && aligned16(r) && (BASE > 2 || aligned16(y)) && n % E == 0;
+  const bool vec = aligned32(x) && aligned32(r) && (BASE > 2 || aligned32(y)) && n % E == 0;
   if (vec) {
-    int64_t nvec = n / E;
-    int64_t blocks = (nvec / 4 + 255) / 256;
+    const int64_t nvec = n / E;
+    int64_t blocks = (nvec + 511) / 512;
     blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
     dotted_vec_kernel<T, BASE><<<(unsigned)blocks, 256, 0, s>>>(
-        static_cast<const typename Vec16<T>::type*>(x),
-        static_cast<const typename Vec16<T>::type*>(y ? y : x),
-        static_cast<typename Vec16<T>::type*>(r), nvec);
+        static_cast<const Vec32<T>*>(x), static_cast<const Vec32<T>*>(y ? y : x),
+        static_cast<Vec32<T>*>(r), nvec);
   } else {
     int64_t blocks = (n + 255) / 256;
     blocks = blocks < 1 ? 1 : (blocks > cap ? cap : blocks);
