@@ -63,43 +63,94 @@ __device__ __forceinline__ void st2(T* v, T* e, int64_t i, TF<T> z) {
   st_stream(e + i, z.b);
 }
 
+#ifndef TF_FQUAD_VB
+#define TF_FQUAD_VB 16  // quadratic: 16-byte vectors (6 in + 6 out planes per thread)
+#endif
+
 struct FArgs {
   const void* in[6];
   void* out[6];
 };
 
-template <class T>
-__global__ void __launch_bounds__(256) axpy_kernel(FArgs p, int64_t n, int submul) {
-  const T* const* in = reinterpret_cast<const T* const*>(p.in);
-  T* const* out = reinterpret_cast<T* const*>(p.out);
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gstride) {
-    TF<T> a = ld2(in[0], in[1], i), x = ld2(in[2], in[3], i), y = ld2(in[4], in[5], i);
-    TF<T> z;
-    if (submul) z = Tsub(a, Tmul(x, y));  // a is c here: c - a*b
-    else z = Tadd(Tmul(a, x), y);
-    st2(out[0], out[1], i, z);
+// One instance of a fused chain: v = the 6 input values, z = the outputs.
+template <class T, int FOP>
+__device__ __forceinline__ void fused_elem(const T* v, T* z) {
+  const TF<T> a{v[0], v[1]}, x{v[2], v[3]}, y{v[4], v[5]};
+  if constexpr (FOP == TF_FAXPY) {
+    const TF<T> r = Tadd(Tmul(a, x), y);
+    z[0] = r.a;
+    z[1] = r.b;
+  } else if constexpr (FOP == TF_FSUBMUL) {
+    const TF<T> r = Tsub(a, Tmul(x, y));  // a is c here: c - a*b
+    z[0] = r.a;
+    z[1] = r.b;
+  } else {  // TF_FQUAD: a x^2 + b x + c with (a, b, c) = (a, x, y)
+    const TF<T> four{T(4), T(0)}, two{T(2), T(0)};
+    const TF<T> disc = Tsub(Tmul(x, x), Tmul(Tmul(four, a), y));
+    const TF<T> d = Tsqrt(disc);
+    const TF<T> nb{-x.a, -x.b};  // tneg (arith.py:838-842): exact sign flips
+    const TF<T> two_a = Tmul(two, a);
+    const TF<T> x0 = Tdiv(Tsub(nb, d), two_a);
+    const TF<T> x1 = Tdiv(Tadd(nb, d), two_a);
+    z[0] = d.a;
+    z[1] = d.b;
+    z[2] = x0.a;
+    z[3] = x0.b;
+    z[4] = x1.a;
+    z[5] = x1.b;
   }
 }
 
-template <class T>
-__global__ void __launch_bounds__(256) quad_kernel(FArgs p, int64_t n) {
+// axpy / submul / quadratic over n instances: one VB-byte vector per plane per
+// thread (the twofold kernels' memory design), one CTA per 256 vectors; planes
+// that are not all VB-aligned (and the n % E tail) take the scalar path.
+template <class T, int FOP, int VB>
+__global__ void __launch_bounds__(256) fused_ew_kernel(FArgs p, int64_t n, int64_t nvec) {
+  constexpr int NI = 6, NO = FOP == TF_FQUAD ? 6 : 2;
+  using V = VecN<T, VB>;
+  constexpr int E = V::N;
   const T* const* in = reinterpret_cast<const T* const*>(p.in);
   T* const* out = reinterpret_cast<T* const*>(p.out);
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
-  const TF<T> four{T(4), T(0)}, two{T(2), T(0)};
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gstride) {
-    TF<T> a = ld2(in[0], in[1], i), b = ld2(in[2], in[3], i), c = ld2(in[4], in[5], i);
-    TF<T> disc = Tsub(Tmul(b, b), Tmul(Tmul(four, a), c));
-    TF<T> d = Tsqrt(disc);
-    TF<T> nb{-b.a, -b.b};  // tneg (arith.py:838-842): exact sign flips
-    TF<T> two_a = Tmul(two, a);
-    TF<T> x0 = Tdiv(Tsub(nb, d), two_a);
-    TF<T> x1 = Tdiv(Tadd(nb, d), two_a);
-    st2(out[0], out[1], i, d);
-    st2(out[2], out[3], i, x0);
-    st2(out[4], out[5], i, x1);
+  for (int64_t j = gtid; j < nvec; j += gstride) {
+    V r[NI];
+#pragma unroll
+    for (int k = 0; k < NI; k++) r[k] = ld_stream(reinterpret_cast<const V*>(in[k]) + j);
+    V o[NO];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      T v[NI], z[NO];
+#pragma unroll
+      for (int k = 0; k < NI; k++) v[k] = r[k].v[e];
+      fused_elem<T, FOP>(v, z);
+#pragma unroll
+      for (int k = 0; k < NO; k++) o[k].v[e] = z[k];
+    }
+#pragma unroll
+    for (int k = 0; k < NO; k++) st_stream(reinterpret_cast<V*>(out[k]) + j, o[k]);
   }
+  for (int64_t i = nvec * E + gtid; i < n; i += gstride) {
+    T v[NI], z[NO];
+#pragma unroll
+    for (int k = 0; k < NI; k++) v[k] = ld_stream(in[k] + i);
+    fused_elem<T, FOP>(v, z);
+#pragma unroll
+    for (int k = 0; k < NO; k++) st_stream(out[k] + i, z[k]);
+  }
+}
+
+template <class T, int FOP, int VB>
+static void launch_fused_ew(const FArgs& p, int64_t n, cudaStream_t s) {
+  constexpr int E = VecN<T, VB>::N;
+  constexpr int NO = FOP == TF_FQUAD ? 6 : 2;
+  bool aligned = true;
+  for (int k = 0; k < 6; k++) aligned = aligned && (reinterpret_cast<uintptr_t>(p.in[k]) % VB == 0);
+  for (int k = 0; k < NO; k++) aligned = aligned && (reinterpret_cast<uintptr_t>(p.out[k]) % VB == 0);
+  const int64_t nvec = aligned ? n / E : 0;
+  int64_t blocks = nvec > 0 ? (nvec + 255) / 256 : (n + 255) / 256;
+  blocks = blocks > 0x7fffffffLL ? 0x7fffffffLL : (blocks < 1 ? 1 : blocks);
+  fused_ew_kernel<T, FOP, VB><<<(unsigned)blocks, 256, 0, s>>>(p, n, nvec);
 }
 
 template <class T>
@@ -157,19 +208,22 @@ int fused_launch(int fop, int dtype, int64_t n, const void* const* in, void* con
   FArgs p{};
   for (int k = 0; k < nin[fop]; k++) p.in[k] = in[k];
   for (int k = 0; k < nout[fop]; k++) p.out[k] = out[k];
-  const int threads = fop == 3 ? 128 : 256;
+  const int threads = 128;  // gauss3 (the others: launch_fused_ew)
   int64_t blocks = (n + threads - 1) / threads;
   blocks = blocks > 0x7fffffffLL ? 0x7fffffffLL : blocks;  // one CTA per chunk
   const bool f64 = dtype == TF_F64;
   switch (fop) {
-    case 0:
-    case 1:
-      if (f64) axpy_kernel<double><<<(unsigned)blocks, threads, 0, s>>>(p, n, fop);
-      else axpy_kernel<float><<<(unsigned)blocks, threads, 0, s>>>(p, n, fop);
+    case TF_FAXPY:
+      if (f64) launch_fused_ew<double, TF_FAXPY, 32>(p, n, s);
+      else launch_fused_ew<float, TF_FAXPY, 32>(p, n, s);
       break;
-    case 2:
-      if (f64) quad_kernel<double><<<(unsigned)blocks, threads, 0, s>>>(p, n);
-      else quad_kernel<float><<<(unsigned)blocks, threads, 0, s>>>(p, n);
+    case TF_FSUBMUL:
+      if (f64) launch_fused_ew<double, TF_FSUBMUL, 32>(p, n, s);
+      else launch_fused_ew<float, TF_FSUBMUL, 32>(p, n, s);
+      break;
+    case TF_FQUAD:
+      if (f64) launch_fused_ew<double, TF_FQUAD, TF_FQUAD_VB>(p, n, s);
+      else launch_fused_ew<float, TF_FQUAD, TF_FQUAD_VB>(p, n, s);
       break;
     default:
       if (f64)
