@@ -130,3 +130,33 @@ def test_gpu_fused_large_matches_composition():
     K.vtadd2(t, K.TwofoldArray(y0, y1), want)
     z = F.vtaxpy(a, K.TwofoldArray(x0, x1), K.TwofoldArray(y0, y1))
     assert torch.equal(z.value, want.value) and torch.equal(z.error, want.error)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", FMTS)
+@pytest.mark.parametrize("offset", [1, 2])
+def test_gpu_fused_misaligned_and_tails_match_aligned(fmt, offset):
+    # the vector body needs every plane aligned to the vector width; shifted
+    # views take the scalar path, odd n leaves a scalar tail — bits unchanged
+    import torch
+
+    from paper_1401_6235_b200 import fused as F
+    from paper_1401_6235_b200.kernels import TwofoldArray as TA
+
+    dt = torch.float64 if fmt == "f64" else torch.float32
+    n = 4099
+    rng = np.random.default_rng(3)
+    base = [rng.uniform(0.5, 2.0, n + offset) for _ in range(6)]
+    base[4] *= 0.1  # c small: real roots for the quadratic
+
+    mis = [torch.as_tensor(b, dtype=dt, device="cuda")[offset:offset + n] for b in base]
+    al = [m.clone() for m in mis]  # the same values in fresh (aligned) allocations
+    for fn in (F.vtaxpy, F.vtsubmul):
+        za = fn(TA(al[0], al[1]), TA(al[2], al[3]), TA(al[4], al[5]))
+        zm = fn(TA(mis[0], mis[1]), TA(mis[2], mis[3]), TA(mis[4], mis[5]))
+        assert torch.equal(za.value, zm.value) and torch.equal(za.error, zm.error)
+    qa = F.vtquadratic(TA(al[0], al[1]), TA(al[2], al[3]), TA(al[4], al[5]))
+    qm = F.vtquadratic(TA(mis[0], mis[1]), TA(mis[2], mis[3]), TA(mis[4], mis[5]))
+    for a, m in zip(qa, qm):
+        assert bits_equal(np.stack([a.value.cpu().numpy(), a.error.cpu().numpy()]),
+                          np.stack([m.value.cpu().numpy(), m.error.cpu().numpy()]))
