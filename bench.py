@@ -986,6 +986,37 @@ def run_config4(args, rank, world, local):
     dot_ms = sum(a.elapsed_time(b) for a, b in ev) / K
     peak, src = measured_peak()
     value = world * 2 * n * K / (elapsed_ms * 1e-3)
+    # the step's two reductions as ONE pass over x and y (reduce.batch ->
+    # tf_reduce_pair): x is read once, 16 instead of 24 bytes per element
+    dbatch = None
+    if not args.no_device_batch:
+        pair_out = torch.empty((2, 2), dtype=torch.float64, device="cuda")
+        calls = [("vtdot", X, Y), ("vtsum", X)]
+        for _ in range(max(1, args.warmup)):
+            R.batch(calls, out=pair_out)
+        bev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(K)]
+        barrier(world)
+        torch.cuda.synchronize()
+        for s_ in range(K):
+            bev[s_][0].record(stream)
+            R.batch(calls, out=pair_out)
+            if world > 1:
+                cross(pair_out[0])
+                cross(pair_out[1])
+            bev[s_][1].record(stream)
+        torch.cuda.synchronize()
+        bms = max_over_ranks(sum(a.elapsed_time(b) for a, b in bev), world) / K
+        same = pair_out.cpu().tolist() == [part.cpu().tolist(), part2.cpu().tolist()]
+        bgbs = 16 * n / (bms * 1e-3) / 1e9
+        dbatch = {"value": world * 2 * n / (bms * 1e-3), "unit": "elem-ops/s", "ms_per_step": bms,
+                  "bytes_per_step": 16 * n,
+                  "roofline": {"bound": "hbm", "achieved": bgbs, "peak": peak, "unit": "GB/s",
+                               "frac": bgbs / peak},
+                  "launches_per_step": 1 + (4 if world > 1 else 0),
+                  "same_bits_as_separate_reductions": same,
+                  "path": "reduce.batch([vtdot(x, y), vtsum(x)]) -> tf_reduce_pair: one pass, "
+                          "both canonical-order reductions, x read once"}
     # e2e: the public API on pinned numpy planes (tf_reduce_host: chunked H2D of
     # complete subtrees + on-device combine; 16 bytes come back per reduction)
     xh, yh = x.numpy(), y.numpy()
@@ -1038,6 +1069,7 @@ def run_config4(args, rank, world, local):
                                  "h2d_bytes_per_step": 24 * n, "d2h_bytes_per_step": 32}},
             "cpu_baseline": cpu,
             "gpu_launches": world * K * (2 + (2 if world > 1 and tp is None else 0)),
+            "device_batch": dbatch,
             "reduce_transport": (args.reduce_transport if world > 1 else
                                  "p2p (fused reduce + mailbox exchange, 1 rank)" if tp is not None
                                  else "none (1 GPU)"),

@@ -50,6 +50,7 @@ def _bind(L: ctypes.CDLL) -> None:
         "tf_reduce_geometry": (ci, [ci, ctypes.POINTER(ci), ctypes.POINTER(ci), ctypes.POINTER(ci)]),
         "tf_reduce_workspace_bytes": (ctypes.c_size_t, [ci, ci, i64]),
         "tf_reduce": (ci, [ci, ci, i64, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+        "tf_reduce_pair": (ci, [ci, ci, ci, i64, vp, vp, vp, vp, ctypes.c_size_t, vp]),
         "tf_combine": (ci, [ci, ci, vp, ctypes.POINTER(i64), vp, vp]),
         "tf_reduce_host": (ci, [ci, ci, i64, vp, vp, vp, ci]),
         "tf_reduce_host_batch": (ci, [ci, ctypes.POINTER(ci), ci, i64, vp, vp, vp, ci]),
@@ -81,7 +82,7 @@ def _bind(L: ctypes.CDLL) -> None:
 EXPORTS = (
     "tf_abi_version", "tf_last_error", "tf_num_inputs", "tf_selftest", "tf_elementwise",
     "tf_elementwise_host", "tf_elementwise_host_batch", "tf_elementwise_batch", "tf_host_register", "tf_host_unregister", "tf_elementwise_il", "tf_fused", "tf_interleave", "tf_deinterleave",
-    "tf_reduce_geometry", "tf_reduce_workspace_bytes", "tf_reduce",
+    "tf_reduce_geometry", "tf_reduce_workspace_bytes", "tf_reduce", "tf_reduce_pair",
     "tf_combine", "tf_reduce_host", "tf_reduce_host_batch", "tf_xgpu_mailbox", "tf_xgpu_open", "tf_xgpu_combine",
     "tf_xgpu_status", "tf_xgpu_emulate", "tf_xgpu_reduce", "tf_xgpu_reduce_emulate",
     "tf_xgpu_publish", "tf_xgpu_reduce_publish", "tf_xgpu_collect", "tf_horner", "tf_horner_host", "tf_fill", "tf_dotted", "tf_fp64_peak", "tf_gen_dot_host",

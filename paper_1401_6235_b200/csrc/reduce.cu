@@ -39,6 +39,16 @@ __global__ void __launch_bounds__(RW) reduce_kernel(const T* __restrict__ a,
   reduce_tile<T, ROP, VEC>(a, b, n, ntiles, tiles, counter, out, blockIdx.x);
 }
 
+// ---- two reductions over the same planes in one pass (tf_reduce_pair) -----------
+template <class T, int R1, int R2, bool VEC>
+__global__ void __launch_bounds__(RW) reduce_pair_kernel(const T* __restrict__ a,
+                                                         const T* __restrict__ b, int64_t n,
+                                                         int64_t ntiles, P<T>* tiles1,
+                                                         P<T>* tiles2, unsigned* counter,
+                                                         T* out1, T* out2) {
+  reduce_tile2<T, R1, R2, VEC>(a, b, n, ntiles, tiles1, tiles2, counter, out1, out2, blockIdx.x);
+}
+
 // ---- variant 2: TMA bulk-copy path (cp.async.bulk -> smem ring, mbarriers) ------
 // A tile is streamed through shared memory in stages of KS k-steps (KS*4 KB per
 // plane): one elected thread arms an mbarrier with the byte count and issues
@@ -260,6 +270,53 @@ int reduce_launch(int rop, int dtype, int64_t n, const void* a, const void* b, v
                            : reduce_t<float, ROP>(n, a, b, out, ws, s);
   switch (rop) { R(TF_RSUM) R(TF_RSUM2) R(TF_RDOT) }
 #undef R
+  return TF_EINVAL;
+}
+
+template <class T, int R1, int R2>
+static int reduce_pair_t(int64_t n, const void* a, const void* b, void* out, void* ws,
+                         cudaStream_t s) {
+  const int64_t nt = tiles_for(sizeof(T) == 8 ? TF_F64 : TF_F32, n);
+  unsigned* counter = static_cast<unsigned*>(ws);
+  P<T>* tiles1 = reinterpret_cast<P<T>*>(static_cast<char*>(ws) + 256);
+  P<T>* tiles2 = tiles1 + nt;
+  constexpr bool NEED_B = R1 != TF_RSUM || R2 != TF_RSUM;
+  const bool vec = aligned16(a) && (!NEED_B || aligned16(b));
+  const T* pa = static_cast<const T*>(a);
+  const T* pb = static_cast<const T*>(b ? b : a);
+  T* po = static_cast<T*>(out);
+  if (vec)
+    reduce_pair_kernel<T, R1, R2, true><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles1, tiles2,
+                                                                   counter, po, po + 2);
+  else
+    reduce_pair_kernel<T, R1, R2, false><<<(unsigned)nt, RW, 0, s>>>(pa, pb, n, nt, tiles1,
+                                                                    tiles2, counter, po, po + 2);
+  return launch_status("tf_reduce_pair");
+}
+
+int reduce_pair_launch(int r1, int r2, int dtype, int64_t n, const void* a, const void* b,
+                       void* out, void* ws, size_t ws_bytes, cudaStream_t s) {
+  if (r1 < 0 || r1 >= TF_NUM_ROPS || r2 < 0 || r2 >= TF_NUM_ROPS)
+    return fail(TF_EINVAL, "tf_reduce_pair: unknown reduction id");
+  if (dtype != TF_F32 && dtype != TF_F64)
+    return fail(TF_EINVAL, "tf_reduce_pair: planes must be float32 or float64");
+  if (n < 0) return fail(TF_EINVAL, "tf_reduce_pair: negative length");
+  if (!out) return fail(TF_EINVAL, "tf_reduce_pair: null output");
+  const size_t tsz = dtype == TF_F64 ? 8 : 4;
+  if (n == 0) return cuda_status(cudaMemsetAsync(out, 0, 4 * tsz, s), "tf_reduce_pair: zero");
+  if (!a || ((r1 != TF_RSUM || r2 != TF_RSUM) && !b))
+    return fail(TF_EINVAL, "tf_reduce_pair: null plane");
+  if (!ws || ws_bytes < 2 * reduce_ws_bytes(dtype, n))
+    return fail(TF_EINVAL, "tf_reduce_pair: workspace too small");
+  if (tiles_for(dtype, n) > 0x7fffffffLL) return fail(TF_EINVAL, "tf_reduce_pair: too many tiles");
+#define RP2(A, B)                                                                    \
+  if (r1 == A && r2 == B)                                                            \
+    return dtype == TF_F64 ? reduce_pair_t<double, A, B>(n, a, b, out, ws, s)        \
+                           : reduce_pair_t<float, A, B>(n, a, b, out, ws, s);
+#define RP(A) RP2(A, TF_RSUM) RP2(A, TF_RSUM2) RP2(A, TF_RDOT)
+  RP(TF_RSUM) RP(TF_RSUM2) RP(TF_RDOT)
+#undef RP
+#undef RP2
   return TF_EINVAL;
 }
 

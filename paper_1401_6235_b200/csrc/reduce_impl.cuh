@@ -219,4 +219,124 @@ __device__ __forceinline__ bool reduce_tile(const T* __restrict__ a, const T* __
 }
 
 
+
+// ---- two reductions in one pass -------------------------------------------------
+// Lane fold of two reductions over the same planes (a, b): each accumulator in its
+// own canonical order, so each result is bit-identical to its single reduction;
+// the planes are read once.
+template <class T, int R1, int R2>
+__device__ __forceinline__ void fold2(P<T>& acc1, P<T>& acc2, int& have, T x, T y) {
+  if (!have) {
+    acc1 = first_term<T, R1>(x, y);
+    acc2 = first_term<T, R2>(x, y);
+    have = 1;
+  } else {
+    acc1 = fold<T, R1>(acc1, x, y);
+    acc2 = fold<T, R2>(acc2, x, y);
+  }
+}
+
+// lane trees -> two tile partials; the last CTA (one ticket) runs both tile trees
+template <class T>
+__device__ __forceinline__ bool finish_tile2(P<T> acc1, P<T> acc2, int have, int64_t t,
+                                             int64_t ntiles, P<T>* tiles1, P<T>* tiles2,
+                                             unsigned* counter, T* out1, T* out2) {
+  int h;
+  acc1 = cta_tree(acc1, have, &h);
+  __syncthreads();  // shared scratch of cta_tree is reused
+  acc2 = cta_tree(acc2, have, &h);
+  __shared__ int is_last;
+  if (threadIdx.x == 0) {
+    tiles1[t] = acc1;
+    tiles2[t] = acc2;
+    __threadfence();
+    unsigned prev = atomicAdd(counter, 1u);
+    is_last = (prev == (unsigned)(ntiles - 1));
+  }
+  __syncthreads();
+  if (!is_last) return false;
+  __threadfence();
+  int64_t per = (ntiles + RW - 1) / RW;
+  int64_t B2 = 1;
+  while (B2 < per) B2 <<= 1;
+  const int64_t lo = (int64_t)threadIdx.x * B2;
+  const int64_t hi = lo + B2 < ntiles ? lo + B2 : ntiles;
+  P<T>* const tl[2] = {tiles1, tiles2};
+  T* const outs[2] = {out1, out2};
+#pragma unroll 1
+  for (int r = 0; r < 2; r++) {
+    P<T> part{T(0), T(0)};
+    int ph = 0;
+    if (lo < ntiles) {
+      part = block_tree(tl[r], lo, hi);
+      ph = 1;
+    }
+    __syncthreads();
+    part = cta_tree(part, ph, &h);
+    if (threadIdx.x == 0) {
+      outs[r][0] = part.a;
+      outs[r][1] = part.b;
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+template <class T, int R1, int R2, bool VEC>
+__device__ __forceinline__ bool reduce_tile2(const T* __restrict__ a, const T* __restrict__ b,
+                                             int64_t n, int64_t ntiles, P<T>* tiles1,
+                                             P<T>* tiles2, unsigned* counter, T* out1, T* out2,
+                                             int64_t t) {
+  constexpr int V = Geo<T>::V;
+  constexpr int64_t L = Geo<T>::L;
+  constexpr bool ONE = R1 == TF_RSUM && R2 == TF_RSUM;  // only plane a is read
+  using Vt = typename Vec16<T>::type;
+  const int w = threadIdx.x;
+  const int64_t base = t * L;
+  P<T> acc1{T(0), T(0)}, acc2{T(0), T(0)};
+  int have = 0;
+  if (VEC && base + L <= n) {
+    const Vt* va = reinterpret_cast<const Vt*>(a + base) + w;
+    const Vt* vb = reinterpret_cast<const Vt*>((ONE ? a : b) + base) + w;
+    constexpr int KB = ONE ? TF_RKB_SUM : RKB;
+#pragma unroll 1
+    for (int k0 = 0; k0 < RK; k0 += KB) {
+      Vt ra[KB], rb[ONE ? 1 : KB];
+#pragma unroll
+      for (int kb = 0; kb < KB; kb++) {
+        ra[kb] = ld_stream(va + (int64_t)RW * (k0 + kb));
+        if constexpr (!ONE) rb[kb] = ld_stream(vb + (int64_t)RW * (k0 + kb));
+      }
+#pragma unroll
+      for (int kb = 0; kb < KB; kb++) {
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          T x = lane<T>(ra[kb], e);
+          T y = x;
+          if constexpr (!ONE) y = lane<T>(rb[kb], e);
+          if (k0 == 0 && kb == 0 && e == 0) {
+            acc1 = first_term<T, R1>(x, y);
+            acc2 = first_term<T, R2>(x, y);
+          } else {
+            acc1 = fold<T, R1>(acc1, x, y);
+            acc2 = fold<T, R2>(acc2, x, y);
+          }
+        }
+      }
+    }
+    have = 1;
+  } else {
+    for (int k = 0; k < RK; k++) {
+      for (int e = 0; e < V; e++) {
+        const int64_t i = base + (int64_t)V * (w + (int64_t)RW * k) + e;
+        if (i >= n) continue;
+        T x = ld_stream(a + i);
+        T y = ONE ? x : ld_stream(b + i);
+        fold2<T, R1, R2>(acc1, acc2, have, x, y);
+      }
+    }
+  }
+  return finish_tile2(acc1, acc2, have, t, ntiles, tiles1, tiles2, counter, out1, out2);
+}
+
 }  // namespace tf

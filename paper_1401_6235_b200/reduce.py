@@ -54,8 +54,8 @@ def tile_elems(dtype=np.float64) -> int:
     return V * W * K
 
 
-def workspace(device: int, dtype_id: int, n: int, stream=None):
-    need = _lib.lib().tf_reduce_workspace_bytes(0, dtype_id, n)
+def workspace(device: int, dtype_id: int, n: int, stream=None, factor: int = 1):
+    need = factor * _lib.lib().tf_reduce_workspace_bytes(0, dtype_id, n)
     stream = stream if stream is not None else torch.cuda.current_stream(device)
     key = (device, dtype_id, stream.cuda_stream)
     ws = _WS.get(key)
@@ -184,6 +184,82 @@ def host_batch(calls, device=None):
     return [Twofold(float(r[0]), float(r[1])) for r in res]
 
 
+_RED_NAMES = {"vtsum": "sum", "vtsum2": "sum2", "vtdot": "dot"}
+
+
+def _red_call(call):
+    name = call[0]
+    if name not in _RED_NAMES:
+        raise ValueError("batch: unknown reduction %r" % (name,))
+    ins = tuple(call[1]) if name == "vtsum2" else tuple(call[1:])
+    if len(ins) != (1 if name == "vtsum" else 2):
+        raise ValueError("%s: wrong number of planes" % name)
+    return name, _RED_NAMES[name], ins
+
+
+def batch(calls, out=None):
+    """Several reductions over the same CUDA planes, two per pass.
+
+    ``calls`` as for ``host_batch`` (numpy planes are routed there).  Two
+    consecutive calls that read the same plane(s), e.g. ``[("vtdot", x, y),
+    ("vtsum", x)]``, run as ONE kernel (tf_reduce_pair) that reads each plane
+    once; any other call runs on its own.  Each result is bit-identical to its
+    single reduction.  Returns a list of ``Twofold``, or with ``out`` (a
+    (len(calls), 2) CUDA tensor) fills it asynchronously and returns it.
+    """
+    if not calls:
+        return [] if out is None else out
+    parsed = [_red_call(c) for c in calls]
+    descs = [[_describe(name, p) for p in ins] for name, _, ins in parsed]
+    kinds = {d.kind for ds in descs for d in ds}
+    if kinds == {"host"}:
+        if out is not None:
+            raise ValueError("batch: out= is for CUDA planes")
+        return host_batch(calls)
+    if kinds != {"cuda"}:
+        raise ValueError("batch: planes mix host arrays and CUDA tensors")
+    first = descs[0][0]
+    for (name, _, _), ds in zip(parsed, descs):
+        for d in ds:
+            if d.dtype != first.dtype or d.n != first.n or d.device != first.device:
+                raise ValueError("%s: batch planes mix dtypes, lengths or devices" % name)
+    dev, dt, n = first.device, _dtype_id(first.dtype), first.n
+    _lib.ensure_device(dev)
+    tdt = torch.float64 if dt == _lib.TF_F64 else torch.float32
+    res = out if out is not None else torch.empty((len(calls), 2), dtype=tdt,
+                                                  device="cuda:%d" % dev)
+    if res.dtype != tdt or not res.is_cuda or tuple(res.shape) != (len(calls), 2) \
+            or not res.is_contiguous():
+        raise ValueError("batch: out must be a contiguous (len(calls), 2) CUDA tensor")
+    L = _lib.lib()
+    i = 0
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev)
+        while i < len(calls):
+            a1 = descs[i]
+            pair = None
+            if i + 1 < len(calls):
+                a2 = descs[i + 1]
+                b = [ds[1].ptr for ds in (a1, a2) if len(ds) > 1]
+                if a1[0].ptr == a2[0].ptr and len(set(b)) <= 1:
+                    pair = b[0] if b else None
+            if pair is not None or (i + 1 < len(calls) and a1[0].ptr == descs[i + 1][0].ptr
+                                    and len(a1) == len(descs[i + 1]) == 1):
+                ws = workspace(dev, dt, max(n, 1), stream, factor=2)
+                rc = L.tf_reduce_pair(_lib.ROP_IDS[parsed[i][1]], _lib.ROP_IDS[parsed[i + 1][1]],
+                                      dt, n, a1[0].ptr, pair, res[i].data_ptr(), ws.data_ptr(),
+                                      ws.numel(), stream.cuda_stream)
+                _lib.check(rc, "batch")
+                i += 2
+            else:
+                name, rop, ins = parsed[i]
+                _reduce(name, rop, ins, out=res[i])
+                i += 1
+    if out is not None:
+        return out
+    return [Twofold(v[0], v[1]) for v in res.cpu().tolist()]
+
+
 def combine(partials, counts, out=None):
     """Adjacent-pair ``_tadd`` tree over per-shard partials (g x 2 CUDA tensor)."""
     p = partials.contiguous()
@@ -235,5 +311,6 @@ def binomial_coeffs(degree=20):
     return [float((-1) ** (degree - k) * comb(degree, k)) for k in range(degree + 1)]
 
 
-__all__ = ["Twofold", "vtsum", "vtsum2", "vtdot", "vthorner", "combine", "host_batch", "geometry",
+__all__ = ["Twofold", "vtsum", "vtsum2", "vtdot", "vthorner", "combine", "host_batch", "batch",
+           "geometry",
            "tile_elems", "binomial_coeffs", "TwofoldArray"]

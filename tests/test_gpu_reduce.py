@@ -573,3 +573,55 @@ def test_concurrent_threads_and_streams(oracle):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("tdt", [torch.float64, torch.float32])
+def test_reduce_pair_every_combination_matches_single(tdt):
+    # tf_reduce_pair: two reductions in one pass; each result must be the single
+    # reduction's bits — every (rop1, rop2), full and partial tiles, unaligned
+    # views (scalar path), n = 1 and n = 0
+    from paper_1401_6235_b200 import reduce as R
+
+    rng = np.random.default_rng(17)
+    single = {"vtsum": lambda x, y: R.vtsum(x), "vtsum2": lambda x, y: R.vtsum2((x, y)),
+              "vtdot": lambda x, y: R.vtdot(x, y)}
+    call = {"vtsum": lambda x, y: ("vtsum", x), "vtsum2": lambda x, y: ("vtsum2", (x, y)),
+            "vtdot": lambda x, y: ("vtdot", x, y)}
+    for n in (3 * 131072 + 4099, 65536 * 2, 1, 0):
+        base_x = _t(rng.uniform(-1, 1, n + 1) * np.exp2(rng.integers(-30, 31, n + 1))).to(tdt)
+        base_y = _t(rng.uniform(-1, 1, n + 1)).to(tdt)
+        for x, y in ((base_x[:n], base_y[:n]), (base_x[1:], base_y[1:])):
+            for r1 in single:
+                for r2 in single:
+                    got = R.batch([call[r1](x, y), call[r2](x, y)])
+                    want = [single[r1](x, y), single[r2](x, y)]
+                    assert [tuple(g) for g in got] == [tuple(w) for w in want], (n, r1, r2)
+
+
+def test_reduce_batch_config4_ill_conditioned_and_routing(oracle):
+    # config 4's step as one pass on an ill-conditioned dot; non-pairable calls
+    # fall back to single launches; host planes route to host_batch
+    from paper_1401_6235_b200 import reduce as R
+
+    n = (1 << 21) + 77
+    x, y = _ill_dot(n, 1e16, 11)
+    X, Y = _t(x), _t(y)
+    zd, zs = R.batch([("vtdot", X, Y), ("vtsum", X)])
+    assert tuple(zd) == tuple(R.vtdot(X, Y)) and tuple(zs) == tuple(R.vtsum(X))
+    w = oracle.reduce("dot", x, y, geometry=_geom(np.float64))
+    assert tuple(zd) == (float(w[0]), float(w[1]))
+    ok, err, s, t = oracle.bound_ok(zd.value, zd.error, "dot", x, y)
+    assert ok
+    Z = _t(np.ascontiguousarray(y[::-1]))
+    got = R.batch([("vtsum", Y), ("vtdot", X, Y), ("vtsum", Z), ("vtsum", Z)])
+    want = [R.vtsum(Y), R.vtdot(X, Y), R.vtsum(Z), R.vtsum(Z)]
+    assert [tuple(g) for g in got] == [tuple(v) for v in want]
+    out = torch.empty((2, 2), dtype=torch.float64, device=DEV)
+    R.batch([("vtdot", X, Y), ("vtsum", X)], out=out)
+    assert out.cpu().tolist() == [list(zd), list(zs)]
+    hz = R.batch([("vtdot", x, y), ("vtsum", x)])
+    assert [tuple(v) for v in hz] == [tuple(zd), tuple(zs)]
+    with pytest.raises(ValueError, match="mix"):
+        R.batch([("vtdot", X, Y), ("vtsum", X.float())])
+    with pytest.raises(ValueError, match="unknown"):
+        R.batch([("vtnope", X)])
