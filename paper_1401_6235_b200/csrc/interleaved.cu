@@ -49,8 +49,12 @@ __device__ __forceinline__ void il_gather(const ILArgs<T>& p, int64_t i, T* v) {
   }
 }
 
+#ifndef TF_IL_MIN_BLOCKS
+#define TF_IL_MIN_BLOCKS 4  // <= 64 registers: vtmul1 f64 otherwise took 122 (2 CTAs/SM)
+#endif
+
 template <class T, int OP>
-__global__ void __launch_bounds__(256) ew_il_kernel(ILArgs<T> p, int64_t n, int vec) {
+__global__ void __launch_bounds__(256, TF_IL_MIN_BLOCKS) ew_il_kernel(ILArgs<T> p, int64_t n, int vec) {
   constexpr int NIN = OpInfo<OP>::NIN;
   constexpr int AR = OpInfo<OP>::ARITY;
   constexpr int E = Vec16<T>::N;
@@ -65,13 +69,19 @@ __global__ void __launch_bounds__(256) ew_il_kernel(ILArgs<T> p, int64_t n, int 
   using VP = Vec32<T>;   // E pairs
   using VS = Vec16A<T>;  // E scalars
   constexpr bool XP = (AR == 22 || AR == 21 || AR == 2);
-  constexpr int U = 2;  // steps in flight per thread: all loads issue before any math
-  for (int64_t base = gtid; base < nvec; base += gstride * U) {
+  // steps in flight per thread (all loads issue before any math); the one-plane
+  // op (vtsqrt: 16 bytes in per step) carries 4 to keep enough bytes in flight
+  constexpr int U = AR == 1 ? 4 : 2;
+  // CTA-chunked, as the split kernels: chunk = 256*U consecutive steps per CTA,
+  // thread t takes steps t and t+256 (coalesced, contiguous per CTA)
+  const int64_t CH = 256LL * U;
+  for (int64_t cb = (int64_t)blockIdx.x * CH; cb < nvec; cb += (int64_t)gridDim.x * CH) {
+    const int64_t base = cb + threadIdx.x;
     VP xp[U], yp[U];
     VS xs[U], ys[U];
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const int64_t j = base + u * gstride;
+      const int64_t j = base + u * 256;
       if (j < nvec) {
         if constexpr (XP) xp[u] = ld_stream(reinterpret_cast<const VP*>(p.a) + j);
         else xs[u] = ld_stream(reinterpret_cast<const VS*>(p.a) + j);
@@ -81,7 +91,7 @@ __global__ void __launch_bounds__(256) ew_il_kernel(ILArgs<T> p, int64_t n, int 
     }
 #pragma unroll
     for (int u = 0; u < U; u++) {
-      const int64_t j = base + u * gstride;
+      const int64_t j = base + u * 256;
       if (j >= nvec) continue;
       VP o;
 #pragma unroll
@@ -229,7 +239,8 @@ int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* 
   const int E = dtype == TF_F64 ? 2 : 4;
   ILArgs<double> p{static_cast<const double*>(a), static_cast<const double*>(b ? b : a),
                    static_cast<double*>(out)};
-  const int64_t blocks = grid_for(vec ? (n / E + 1) / 2 : n);
+  const int U = ar == 1 ? 4 : 2;  // steps per thread, as in ew_il_kernel
+  const int64_t blocks = grid_for(vec ? (n / E + U - 1) / U : n);
   void* args[] = {&p, &n, &vec};
   return cuda_status(cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, s),
                      "tf_elementwise_il: launch");
