@@ -61,6 +61,29 @@ for dt in (np.float64, np.float32):
     po = torch.empty_like(p)
     IL.vtadd2(p, p, po)
     F.vtaxpy(K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)))
+# device batch (one launch, shared planes) and reduction pairs (one pass)
+for dt in (np.float64, np.float32):
+    for n in (37, 4099, 3 * 65536 + 11):
+        for off in (0, 1):
+            ins = [rng.uniform(0.5, 2, n).astype(dt) for _ in range(4)]
+            P = [put(a, off) for a in ins]
+            X, Y = K.TwofoldArray(P[0], P[1]), K.TwofoldArray(P[2], P[3])
+            outs = [K.TwofoldArray(put(np.zeros(n, dt), off), put(np.zeros(n, dt), off)) for _ in range(3)]
+            K.batch([("vtadd2", X, Y, outs[0]), ("vtdiv2", X, Y, outs[1]), ("vtsqrt1", X, outs[2])])
+            for name, o_, w in (("vtadd2", outs[0], o.elementwise("vtadd2", *ins)),
+                                ("vtdiv2", outs[1], o.elementwise("vtdiv2", *ins)),
+                                ("vtsqrt1", outs[2], o.elementwise("vtsqrt1", ins[0], ins[1]))):
+                if not (np.array_equal(o_.value.cpu().numpy(), w[0]) and
+                        np.array_equal(o_.error.cpu().numpy(), w[1])):
+                    bad += 1
+                    print("batch mismatch", name, dt, n, off)
+            zd, zs = R.batch([("vtdot", P[0], P[2]), ("vtsum", P[0])])
+            geo = R.geometry(dt)
+            wd = o.reduce("dot", ins[0], ins[2], geometry=geo)
+            wsum = o.reduce("sum", ins[0], geometry=geo)
+            if tuple(zd) != (float(wd[0]), float(wd[1])) or tuple(zs) != (float(wsum[0]), float(wsum[1])):
+                bad += 1
+                print("reduce pair mismatch", dt, n, off)
 # host-plane pipeline (pinned and pageable), several chunks
 for dt in (np.float64, np.float32):
     n = 3 * (1 << 18) + 5
