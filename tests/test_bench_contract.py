@@ -63,3 +63,52 @@ def test_exact_check_of_a_generated_dot(oracle):
     assert c["vtdot"]["bound_ok"] and c["vtsum"]["bound_ok"]
     assert 0.5e16 < c["vtdot"]["cond"] < 2e16
     assert c["vtdot"]["z0_plus_z1_rel_err"] < 1e-10 < c["vtdot"]["z0_rel_err"]
+
+
+REQUIRED = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+            "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+            "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("workload", ["config2", "config4", "config5"])
+def test_our_arm_json_line_contract(workload):
+    # the driver's contract on our arm, at a small size: one JSON line with every
+    # required key, the roofline / cpu_baseline / e2e / clocks objects filled, and
+    # the full-size checks of the timed outputs passing
+    elems = {"config2": 1 << 22, "config4": 1 << 23, "config5": 1 << 22}[workload]
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--workload", workload,
+                        "--elems", str(elems), "--steps", "3", "--warmup", "3",
+                        "--cpu-sample", str(1 << 20), "--e2e-steps", "1"],
+                       capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in REQUIRED:
+        assert k in d, k
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3
+    assert d["scaling"] == "weak" and d["higher_is_better"] is True
+    assert "workload" in d["config"]
+    rl = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in rl, k
+    assert rl["achieved"] > 0 and rl["peak"] > 0
+    cb = d["cpu_baseline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in cb, k
+    e = d["e2e"]
+    for k in ("value", "unit", "h2d_bytes_per_step", "d2h_bytes_per_step"):
+        assert k in e, k
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["gpu_launches"] > 0
+    for k in ("sm_mhz", "sm_max_mhz", "reasons"):
+        assert k in d["clocks"], k
+    if workload == "config2":
+        chk = d["device_batch"]["check"]
+        assert all(v for op, c in chk.items() if op != "how" for v in c.values()), chk
+    elif workload == "config4":
+        assert d["device_batch"]["same_bits_as_separate_reductions"] is True
+        assert d["cpu_baseline"]["check"]["vtdot"]["bound_ok"] is True
+    else:
+        assert d["check"]["flag_rate"] > 0.99
