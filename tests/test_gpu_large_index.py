@@ -67,3 +67,19 @@ def test_device_batch_past_2g_elements():
     K.vtsqrt(xs, wb)
     assert torch.equal(a.value[idx], wa.value) and torch.equal(a.error[idx], wa.error)
     assert torch.equal(b.value[idx], wb.value) and torch.equal(b.error[idx], wb.error)
+
+
+def test_reduce_pair_past_2g_elements():
+    # the one-pass dot + sum (tf_reduce_pair) past 2^31 elements: bit-identical
+    # to the two single reductions (64-bit tile and element indexing)
+    from paper_1401_6235_b200 import reduce as R
+    from paper_1401_6235_b200 import workloads as W
+
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40e9:
+        pytest.skip("needs ~40 GB of free HBM")
+    x = W.fill(torch.empty(N, dtype=torch.float32, device="cuda"), W.LOGU_SIGNED, 31, 0, -20.0, 20.0)
+    y = W.fill(torch.empty(N, dtype=torch.float32, device="cuda"), W.UNIFORM, 32, 0, -1.0, 1.0)
+    zd, zs = R.batch([("vtdot", x, y), ("vtsum", x)])
+    assert tuple(zd) == tuple(R.vtdot(x, y))
+    assert tuple(zs) == tuple(R.vtsum(x))
