@@ -398,11 +398,14 @@ def test_cuda_graph_capture_and_replay(oracle):
     o3, o4 = K.empty_twofold(n, torch.float64), K.empty_twofold(n, torch.float64)
     s = torch.cuda.Stream()
 
+    pair = torch.empty((2, 2), dtype=torch.float64, device=DEV)
+
     def step():
         K.vtdiv2(X, Y, o1)
         K.vtadd2(o1, Y, o2)
         R.vtdot(o2.value, Y.value, out=red)
         K.batch([("vtdiv2", X, Y, o3), ("vtmul2", o2, Y, o4)])  # one launch
+        R.batch([("vtdot", o2.value, Y.value), ("vtsum", o2.value)], out=pair)  # one pass
 
     with torch.cuda.stream(s):  # warm (self-test, occupancy, workspace) outside capture
         step()
@@ -411,7 +414,7 @@ def test_cuda_graph_capture_and_replay(oracle):
     with torch.cuda.graph(g, stream=s):
         step()
     for buf in (o1.value, o1.error, o2.value, o2.error, red, o3.value, o3.error,
-                o4.value, o4.error):
+                o4.value, o4.error, pair):
         buf.fill_(7.0)
     g.replay()
     g.replay()
@@ -422,6 +425,8 @@ def test_cuda_graph_capture_and_replay(oracle):
     assert bits_equal(o2.value.cpu().numpy(), w2[0]) and bits_equal(o2.error.cpu().numpy(), w2[1])
     wr = oracle.reduce("dot", w2[0], ins[2], geometry=R.geometry(np.float64))
     assert (red[0].item(), red[1].item()) == (float(wr[0]), float(wr[1]))
+    ws = oracle.reduce("sum", w2[0], geometry=R.geometry(np.float64))
+    assert pair.cpu().tolist() == [[float(wr[0]), float(wr[1])], [float(ws[0]), float(ws[1])]]
     w4 = oracle.elementwise("vtmul2", w2[0], w2[1], ins[2], ins[3])
     assert bits_equal(o3.value.cpu().numpy(), w1[0]) and bits_equal(o3.error.cpu().numpy(), w1[1])
     assert bits_equal(o4.value.cpu().numpy(), w4[0]) and bits_equal(o4.error.cpu().numpy(), w4[1])
