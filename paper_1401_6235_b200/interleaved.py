@@ -112,11 +112,33 @@ def empty_pairs(n, dtype=torch.float64 if torch else None, device="cuda"):
     return torch.empty((n, 2), dtype=dtype, device=device)
 
 
+def _check_convert(name, planes, pairs):
+    """Validate a split <-> interleaved conversion before any launch: the two
+    1-D planes and the (n, 2) pair array share dtype, length and device, all
+    contiguous CUDA tensors, and the destination overlaps no source."""
+    v = _desc(name, planes[0], False)
+    e = _desc(name, planes[1], False)
+    p = _desc(name, pairs, True)
+    n = p.shape[0]
+    for t in (v, e):
+        if t.dtype != p.dtype:
+            raise ValueError("%s: planes mix %s and %s" % (name, t.dtype, p.dtype))
+        if t.shape[0] != n:
+            raise ValueError("%s: plane lengths differ (%d vs %d)" % (name, t.shape[0], n))
+        if t.device != p.device:
+            raise ValueError("%s: planes live on different devices" % name)
+    return v, e, p, n
+
+
 def from_split(x, out=None):
     """TwofoldArray of CUDA planes -> (n, 2) pair array (tf_interleave)."""
     v, e = x
-    n = v.shape[0]
-    out = out if out is not None else torch.empty((n, 2), dtype=v.dtype, device=v.device)
+    if out is None:
+        _desc("from_split", v, False)
+        out = torch.empty((v.shape[0], 2), dtype=v.dtype, device=v.device)
+    v, e, out, n = _check_convert("from_split", (v, e), out)
+    if _overlap(out, v) or _overlap(out, e):
+        raise ValueError("from_split: out must not alias an input")
     if n:
         dt = _lib.TF_F64 if v.dtype == torch.float64 else _lib.TF_F32
         _lib.ensure_device(v.device.index)
@@ -129,17 +151,23 @@ def from_split(x, out=None):
 
 def to_split(pairs, out=None, kind=TwofoldArray):
     """(n, 2) pair array -> TwofoldArray of CUDA planes (tf_deinterleave)."""
-    n = pairs.shape[0]
     if out is None:
+        _desc("to_split", pairs, True)
+        n = pairs.shape[0]
         out = kind(torch.empty(n, dtype=pairs.dtype, device=pairs.device),
                    torch.empty(n, dtype=pairs.dtype, device=pairs.device))
+    v, e, pairs, n = _check_convert("to_split", (out[0], out[1]), pairs)
+    if _overlap(v, pairs) or _overlap(e, pairs):
+        raise ValueError("to_split: out must not alias an input")
+    if _overlap(v, e):
+        raise ValueError("to_split: out planes overlap each other")
     if n:
         dt = _lib.TF_F64 if pairs.dtype == torch.float64 else _lib.TF_F32
         _lib.ensure_device(pairs.device.index)
         with torch.cuda.device(pairs.device):
             s = torch.cuda.current_stream(pairs.device).cuda_stream
-            _lib.check(_lib.lib().tf_deinterleave(dt, n, pairs.data_ptr(), out[0].data_ptr(),
-                                                  out[1].data_ptr(), s), "to_split")
+            _lib.check(_lib.lib().tf_deinterleave(dt, n, pairs.data_ptr(), v.data_ptr(),
+                                                  e.data_ptr(), s), "to_split")
     return out
 
 

@@ -304,21 +304,27 @@ def _torch_dtype(dt):
     return d
 
 
-def empty_twofold(n, dtype=np.float64, kind=TwofoldArray, device="cuda", pin_memory=False):
+def empty_twofold(n, dtype=np.float64, kind=TwofoldArray, device=None, pin_memory=False):
     """Allocate an uninitialized twofold array of n elements (kernels.py:250-255).
 
-    ``device="cuda"`` (default; or "cuda:k" / an index) allocates CUDA tensors on
-    that device; ``device="cpu"`` allocates numpy planes as the reference does
-    (optionally in pinned memory, the fast host path).
+    The reference's default is kept: a numpy dtype (the default float64) with no
+    ``device`` gives numpy planes, exactly as ``twofold.kernels.empty_twofold``
+    (optionally page-locked with ``pin_memory=True``, the fast host path).  CUDA
+    planes are opt-in: a torch dtype (``torch.float64``) allocates on the
+    current CUDA device, and ``device="cuda"`` / ``"cuda:k"`` / an index picks
+    one explicitly; ``device="cpu"`` forces numpy planes.
     """
     dt = _torch_dtype(dtype)
-    if torch is not None and isinstance(dt, torch.dtype):
+    is_torch_dt = torch is not None and isinstance(dt, torch.dtype)
+    if is_torch_dt:
         tdt = dt
     else:
         tdt = None
         if torch is not None:
             tdt = torch.float64 if dt == np.dtype(np.float64) else torch.float32
-    if device in ("cpu", "host", None):
+    if device is None:
+        device = "cuda" if is_torch_dt else "cpu"
+    if device in ("cpu", "host"):
         if pin_memory and torch is not None:
             planes = [torch.empty(n, dtype=tdt, pin_memory=True).numpy() for _ in range(2)]
             return kind(*planes)
@@ -456,7 +462,11 @@ import weakref as _weakref
 
 _REG_LOCK = _threading.Lock()
 _REG = _collections.OrderedDict()  # owner address -> (nbytes, finalizer)
-_SEEN = {}
+# owner address -> (uses, weakref to the owner).  The weakref ties a count to the
+# array that earned it (a new array at a recycled address starts from zero) and
+# lets dead entries be pruned; the table is capped at _SEEN_MAX live entries.
+_SEEN = _collections.OrderedDict()
+_SEEN_MAX = 256
 _REG_MIN = 32 << 20
 _REG_BUDGET = int(float(_os.environ.get("TF_HOST_REGISTER_GB", "16")) * (1 << 30))
 # page-locking costs ~80 ms per GiB (measured) and saves ~40% of a staged call,
@@ -493,8 +503,17 @@ def _maybe_register(a):
         if addr in _REG:
             _REG.move_to_end(addr)
             return
-        _SEEN[addr] = _SEEN.get(addr, 0) + 1
-        if _SEEN[addr] < _REG_AFTER or o.nbytes > _REG_BUDGET:
+        uses, ref = _SEEN.pop(addr, (0, None))
+        if ref is None or ref() is not o:
+            uses = 0  # first sight, or a new array at a recycled address
+        uses += 1
+        _SEEN[addr] = (uses, _weakref.ref(o))
+        if len(_SEEN) > _SEEN_MAX:
+            for k in [k for k, (_, r) in _SEEN.items() if r() is None]:
+                del _SEEN[k]
+            while len(_SEEN) > _SEEN_MAX:
+                _SEEN.popitem(last=False)
+        if uses < _REG_AFTER or o.nbytes > _REG_BUDGET:
             return
         total = sum(v[0] for v in _REG.values())
         while _REG and total + o.nbytes > _REG_BUDGET:
@@ -503,7 +522,7 @@ def _maybe_register(a):
             (_lib._lib or _lib.lib()).tf_host_unregister(old)
             total -= nb
         if (_lib._lib or _lib.lib()).tf_host_register(addr, o.nbytes) != 0:
-            _SEEN[addr] = -(1 << 30)  # not registrable: stay on the staging path
+            _SEEN[addr] = (-(1 << 30), _weakref.ref(o))  # not registrable: stay staged
             return
         _REG[addr] = (o.nbytes, _weakref.finalize(o, _unregister, addr))
         _SEEN.pop(addr, None)

@@ -38,31 +38,31 @@ Twofold = namedtuple("Twofold", ("value", "error"))
 # zeroed).  Keyed by stream: reductions on different streams may run concurrently
 # and must not share the tile-partial array or the ticket counter.
 _WS = {}
-
-
-def geometry(dtype=np.float64):
-    """(V, W, K) of the canonical order for a plane dtype."""
-    V, W, K = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
-    dt = _lib.TF_F64 if np.dtype(dtype) == np.float64 else _lib.TF_F32
-    _lib.check(_lib.lib().tf_reduce_geometry(dt, ctypes.byref(V), ctypes.byref(W),
-                                             ctypes.byref(K)), "geometry")
-    return V.value, W.value, K.value
-
-
-def tile_elems(dtype=np.float64) -> int:
-    V, W, K = geometry(dtype)
-    return V * W * K
+# Workspaces are never handed back to the allocator while a captured CUDA graph
+# may still reference them: one outgrown by a larger reduction is retired here
+# (kept alive) instead of freed, and a reduction captured into a graph gets a
+# workspace of its own, so graph replays never share a ticket counter with eager
+# reductions (or with another graph) and never write into recycled memory.
+_WS_RETIRED = []
+_WS_CAPTURED = []
 
 
 def workspace(device: int, dtype_id: int, n: int, stream=None, factor: int = 1):
     need = factor * _lib.lib().tf_reduce_workspace_bytes(0, dtype_id, n)
     stream = stream if stream is not None else torch.cuda.current_stream(device)
+    if torch.cuda.is_current_stream_capturing():
+        with torch.cuda.stream(stream):  # allocated and zeroed inside the capture
+            ws = torch.zeros(max(need, 4096), dtype=torch.uint8, device="cuda:%d" % device)
+        _WS_CAPTURED.append(ws)
+        return ws
     key = (device, dtype_id, stream.cuda_stream)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
         with torch.cuda.stream(stream):  # allocated, zeroed and used on one stream
-            ws = torch.zeros(max(need, 4096), dtype=torch.uint8, device="cuda:%d" % device)
-        _WS[key] = ws
+            new = torch.zeros(max(need, 4096), dtype=torch.uint8, device="cuda:%d" % device)
+        if ws is not None:
+            _WS_RETIRED.append(ws)
+        ws = _WS[key] = new
     return ws
 
 
@@ -101,8 +101,10 @@ def _reduce(name, rop, ins, out=None):
     dt = _dtype_id(first.dtype)
     tdt = torch.float64 if dt == _lib.TF_F64 else torch.float32
     res = out if out is not None else torch.empty(2, dtype=tdt, device="cuda:%d" % dev)
-    if res.dtype != tdt or not res.is_cuda or res.numel() < 2:
-        raise ValueError("%s: out must be a 2-element CUDA tensor of the plane dtype" % name)
+    if (res.dtype != tdt or not res.is_cuda or res.numel() < 2 or not res.is_contiguous()
+            or res.get_device() != dev):
+        raise ValueError("%s: out must be a contiguous 2-element CUDA tensor of the plane "
+                         "dtype on the planes' device" % name)
     ws = workspace(dev, dt, first.n)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream(dev).cuda_stream

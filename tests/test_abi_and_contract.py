@@ -183,6 +183,62 @@ def test_empty_twofold_host_and_errors():
         K.empty_twofold(5, np.int32)
 
 
+def test_empty_twofold_defaults_to_numpy_like_the_reference():
+    # reference kernels.py:250-255: numpy planes; test_kernels.py:260-267 asserts
+    # the np.dtype of each plane.  CUDA planes are opt-in (a torch dtype or device=)
+    import torch
+
+    from paper_1401_6235_b200 import kernels as K
+
+    z = K.empty_twofold(5)
+    assert type(z) is K.TwofoldArray and isinstance(z.value, np.ndarray)
+    assert z.value.dtype == np.dtype(np.float64) and z.value.shape == (5,)
+    z = K.empty_twofold(5, np.float32, K.CoupledArray)
+    assert type(z) is K.CoupledArray and isinstance(z.error, np.ndarray)
+    assert z.error.dtype == np.dtype(np.float32)
+    # a torch dtype with device="cpu" still gives numpy planes of that width
+    z = K.empty_twofold(3, torch.float32, device="cpu")
+    assert isinstance(z.value, np.ndarray) and z.value.dtype == np.float32
+
+
+def test_seen_table_is_bounded_and_tied_to_the_array(monkeypatch):
+    # the reuse counter behind page-locking (kernels._maybe_register) keeps at
+    # most _SEEN_MAX entries, and a new array at a recycled address starts at 0
+    from paper_1401_6235_b200 import kernels as K
+
+    monkeypatch.setattr(K, "_REG_MIN", 0)
+    monkeypatch.setattr(K, "_REG_AFTER", 1 << 30)  # never actually page-lock here
+    monkeypatch.setattr(K, "_SEEN", K._collections.OrderedDict())
+    keep = [np.empty(4) for _ in range(3 * K._SEEN_MAX)]
+    for a in keep:
+        K._maybe_register(a)
+    assert len(K._SEEN) <= K._SEEN_MAX
+    a = np.empty(8)
+    for _ in range(3):
+        K._maybe_register(a)
+    assert K._SEEN[a.ctypes.data][0] == 3
+    addr = a.ctypes.data
+    del a
+    b = np.empty(8)
+    K._maybe_register(b)
+    if b.ctypes.data == addr:  # recycled address: the old count does not carry over
+        assert K._SEEN[addr][0] == 1
+
+
+def test_interleaved_conversion_validates_before_launch():
+    # from_split / to_split check planes before passing raw pointers
+    import torch
+
+    from paper_1401_6235_b200 import interleaved as IL
+    from paper_1401_6235_b200 import kernels as K
+
+    v = torch.zeros(8, dtype=torch.float64)
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        IL.from_split(K.TwofoldArray(v, v))
+    with pytest.raises(ValueError, match="CUDA tensors"):
+        IL.to_split(torch.zeros((8, 2), dtype=torch.float64))
+
+
 def test_batch_validation_before_any_launch():
     # kernels.batch / host_batch validate every call (the reference's _check
     # messages) and the batch as a whole before the library is touched

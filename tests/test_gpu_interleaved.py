@@ -136,3 +136,37 @@ def test_interleaved_validation_without_gpu():
         IL.vtadd2(x, x, x)
     with pytest.raises(ValueError, match="CUDA tensors"):
         IL.vtadd2(np.zeros((8, 2)), x, x)
+
+
+@pytest.mark.gpu
+def test_conversions_validate_before_launch():
+    # a short or float32 out, a 1-D pair array or aliasing planes
+    # raise ValueError instead of reaching the kernel with raw pointers
+    from paper_1401_6235_b200 import interleaved as IL
+    from paper_1401_6235_b200 import kernels as K
+
+    v = torch.ones(64, dtype=torch.float64, device="cuda")
+    e = torch.zeros(64, dtype=torch.float64, device="cuda")
+    x = K.TwofoldArray(v, e)
+    with pytest.raises(ValueError, match="lengths differ"):
+        IL.from_split(x, torch.empty((32, 2), dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError, match="mix"):
+        IL.from_split(x, torch.empty((64, 2), dtype=torch.float32, device="cuda"))
+    with pytest.raises(ValueError, match="pair arrays"):
+        IL.from_split(x, torch.empty(128, dtype=torch.float64, device="cuda"))
+    with pytest.raises(ValueError, match="lengths differ"):
+        IL.from_split(K.TwofoldArray(v, e[:10]))
+    buf = torch.empty(256, dtype=torch.float64, device="cuda")
+    with pytest.raises(ValueError, match="alias"):
+        IL.from_split(K.TwofoldArray(buf[:64], e), buf[:128].view(64, 2))
+    p = IL.from_split(x)
+    with pytest.raises(ValueError, match="pair arrays"):
+        IL.to_split(p.reshape(-1))
+    with pytest.raises(ValueError, match="lengths differ"):
+        IL.to_split(p, K.TwofoldArray(torch.empty(10, dtype=torch.float64, device="cuda"),
+                                      torch.empty(64, dtype=torch.float64, device="cuda")))
+    with pytest.raises(ValueError, match="overlap"):
+        same = torch.empty(64, dtype=torch.float64, device="cuda")
+        IL.to_split(p, K.TwofoldArray(same, same))
+    back = IL.to_split(p)
+    assert torch.equal(back.value, v) and torch.equal(back.error, e)

@@ -625,3 +625,51 @@ def test_reduce_batch_config4_ill_conditioned_and_routing(oracle):
         R.batch([("vtdot", X, Y), ("vtsum", X.float())])
     with pytest.raises(ValueError, match="unknown"):
         R.batch([("vtnope", X)])
+
+
+def test_reduce_out_must_be_contiguous_and_on_the_planes_device():
+    # a strided out view (t[:, 0]) would receive the wrong elements
+    from paper_1401_6235_b200 import reduce as R
+
+    x = torch.ones(1000, dtype=torch.float64, device=DEV)
+    t = torch.zeros((2, 2), dtype=torch.float64, device=DEV)
+    with pytest.raises(ValueError, match="contiguous"):
+        R.vtsum(x, out=t[:, 0])
+    with pytest.raises(ValueError, match="2-element"):
+        R.vtsum(x, out=torch.zeros(2, dtype=torch.float64))
+    out = torch.zeros(2, dtype=torch.float64, device=DEV)
+    R.vtsum(x, out=out)
+    assert out.tolist() == [1000.0, 0.0]
+
+
+def test_captured_reduction_keeps_its_workspace_when_the_cache_grows(oracle):
+    # a graph bakes in its workspace address; a later, larger eager
+    # reduction on the same stream must not free it (use-after-free on replay),
+    # and replays must not share a ticket counter with eager reductions
+    from paper_1401_6235_b200 import reduce as R
+
+    rng = np.random.default_rng(77)
+    small = rng.uniform(-1, 1, 3 * 65536 + 5)
+    big = rng.uniform(-1, 1, 64 * 65536 + 3)
+    xs, xb = _t(small), _t(big)
+    s = torch.cuda.Stream()
+    out = torch.zeros(2, dtype=torch.float64, device=DEV)
+    with torch.cuda.stream(s):
+        R.vtsum(xs, out=out)  # warm the per-stream cache at the small size
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        R.vtsum(xs, out=out)
+    with torch.cuda.stream(s):
+        zb = R.vtsum(xb)  # grows the eager workspace of this stream
+        junk = torch.full((1 << 22,), 3.0, dtype=torch.float64, device=DEV)  # reuse freed memory
+    V, W, Kk = R.geometry(np.float64)
+    want_s = oracle.reduce("sum", small, geometry=(V, W, Kk))
+    want_b = oracle.reduce("sum", big, geometry=(V, W, Kk))
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert out.tolist() == [float(want_s[0]), float(want_s[1])]
+    assert (zb.value, zb.error) == (float(want_b[0]), float(want_b[1]))
+    del junk
