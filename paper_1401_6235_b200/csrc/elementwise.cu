@@ -24,6 +24,18 @@
 #include "common.cuh"
 #include "tf_math.cuh"
 
+// minimum resident CTAs requested for the vtsqrt1 vector kernel (A/B builds)
+#ifndef TF_SQRT_MINB
+#define TF_SQRT_MINB 1
+#endif
+// 32-byte vectors in flight per plane per thread for vtsqrt1: 1 (two IEEE square
+// roots and a division per element keep more elements in flight than registers
+// allow: U = 1 holds 56 registers, 4 CTAs per SM; U = 2 held 80-84, 3 CTAs, and
+// ran 13% slower — profiles/r2_sqrt_ab.txt)
+#ifndef TF_SQRT_U
+#define TF_SQRT_U 1
+#endif
+
 namespace tf {
 
 template <class T>
@@ -48,13 +60,39 @@ __device__ __forceinline__ void scalar_elem(const Planes<T>& p, int64_t i) {
   st_stream(p.out[1] + i, z.b);
 }
 
+template <class T, int OP, int VB, int U>
+__device__ __forceinline__ void compute_store(const VecN<T, VB> (&r)[U][OpInfo<OP>::NIN],
+                                              int64_t base, int64_t nvec, VecN<T, VB>* vo0,
+                                              VecN<T, VB>* vo1) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  constexpr int E = VecN<T, VB>::N;
+#pragma unroll
+  for (int u = 0; u < U; u++) {
+    const int64_t j = base + u * 256;
+    if (j < nvec) {
+      VecN<T, VB> o0, o1;
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        T v[NIN];
+#pragma unroll
+        for (int k = 0; k < NIN; k++) v[k] = r[u][k].v[e];
+        P<T> z = apply<T, OP>(v);
+        o0.v[e] = z.a;
+        o1.v[e] = z.b;
+      }
+      st_stream(vo0 + j, o0);
+      st_stream(vo1 + j, o1);
+    }
+  }
+}
+
 template <class T, int OP, int VB>
-__global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t head,
+__global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB : 1) ew_kernel(Planes<T> p, int64_t n, int64_t head,
                                                  int64_t nvec, int reps) {
   constexpr int NIN = OpInfo<OP>::NIN;
   using V = VecN<T, VB>;
   constexpr int E = V::N;
-  constexpr int U = (VB == 32) ? (NIN >= 3 ? 1 : 2) : Unroll<NIN>::U;
+  constexpr int U = (VB == 32) ? (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : 2)) : Unroll<NIN>::U;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
 
@@ -90,24 +128,7 @@ __global__ void __launch_bounds__(256) ew_kernel(Planes<T> p, int64_t n, int64_t
           for (int k = 0; k < NIN; k++) r[u][k] = ld_stream(vin[k] + j);
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; u++) {
-        const int64_t j = base + u * 256;
-        if (j < nvec) {
-          V o0, o1;
-#pragma unroll
-          for (int e = 0; e < E; e++) {
-            T v[NIN];
-#pragma unroll
-            for (int k = 0; k < NIN; k++) v[k] = r[u][k].v[e];
-            P<T> z = apply<T, OP>(v);
-            o0.v[e] = z.a;
-            o1.v[e] = z.b;
-          }
-          st_stream(vo0 + j, o0);
-          st_stream(vo1 + j, o1);
-        }
-      }
+      compute_store<T, OP, VB, U>(r, base, nvec, vo0, vo1);
     }
   }
 }
@@ -125,11 +146,11 @@ struct EwEntry {
 template <class T, int OP, int VB>
 EwEntry make_entry() {
   constexpr int NIN = OpInfo<OP>::NIN;
-  constexpr int U = (VB == 32) ? (NIN >= 3 ? 1 : 2) : Unroll<NIN>::U;
+  constexpr int U = (VB == 32) ? (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : 2)) : Unroll<NIN>::U;
   // one 256*U-vector step per CTA was fastest for every op at 2^27 (6.9-7.0 TB/s
-  // for the 48 B/element ops), except vtsqrt1 (div + 2 sqrt per element): two
-  // steps (profiles/r1s2_chunk_reps_hbm.txt)
-  constexpr int REPS = OP == 12 ? 2 : 1;
+  // for the 48 B/element ops; profiles/r1s2_chunk_reps_hbm.txt), except vtsqrt1
+  // (div + 2 sqrt per element, U = 1): four steps (profiles/r2_sqrt_ab.txt)
+  constexpr int REPS = OP == 12 ? 4 : 1;
   return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>), NIN, U, REPS, {0}};
 }
 

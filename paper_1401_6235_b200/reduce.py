@@ -47,6 +47,20 @@ _WS_RETIRED = []
 _WS_CAPTURED = []
 
 
+def geometry(dtype=np.float64):
+    """(V, W, K) of the canonical order for a plane dtype."""
+    V, W, K = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    dt = _lib.TF_F64 if np.dtype(dtype) == np.float64 else _lib.TF_F32
+    _lib.check(_lib.lib().tf_reduce_geometry(dt, ctypes.byref(V), ctypes.byref(W),
+                                             ctypes.byref(K)), "geometry")
+    return V.value, W.value, K.value
+
+
+def tile_elems(dtype=np.float64) -> int:
+    V, W, K = geometry(dtype)
+    return V * W * K
+
+
 def workspace(device: int, dtype_id: int, n: int, stream=None, factor: int = 1):
     need = factor * _lib.lib().tf_reduce_workspace_bytes(0, dtype_id, n)
     stream = stream if stream is not None else torch.cuda.current_stream(device)
