@@ -57,15 +57,19 @@ def shard_counts(n: int, world: int, tile: int) -> list:
 
 
 def gather_partials(partial, group=None):
-    """All-gather each rank's 2-element partial into a (world, 2) tensor (rank order)."""
+    """All-gather each rank's partial (2 elements, or any small shape, e.g. the
+    (2, 2) dot and sum partials of one step) into a (world, *shape) tensor in
+    rank order — ONE collective however many reductions it carries."""
     world = dist.get_world_size(group)
-    out = torch.empty((world, 2), dtype=partial.dtype, device=partial.device)
+    shape = tuple(partial.shape)
+    out = torch.empty((world,) + shape, dtype=partial.dtype, device=partial.device)
+    src = partial.contiguous()
     if dist.get_backend(group) == "nccl":
-        dist.all_gather_into_tensor(out, partial.reshape(2).contiguous(), group=group)
+        dist.all_gather_into_tensor(out.reshape(world, -1), src.reshape(-1), group=group)
     else:  # gloo (CPU tests, single-GPU dry runs): gather through host tensors
-        src = partial.reshape(2).contiguous().cpu()
-        parts = [torch.empty(2, dtype=partial.dtype) for _ in range(world)]
-        dist.all_gather(parts, src, group=group)
+        host = src.cpu()
+        parts = [torch.empty_like(host) for _ in range(world)]
+        dist.all_gather(parts, host, group=group)
         for r in range(world):
             out[r] = parts[r].to(out.device)
     return out

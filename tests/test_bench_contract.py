@@ -16,7 +16,7 @@ import pytest
 def test_reference_arm_json_line(workload):
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
                         "--workload", workload, "--steps", "2", "--warmup", "1",
-                        "--cpu-sample", "65536"],
+                        "--ref-elems", "65536"],
                        capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert r.returncode == 0, r.stderr
     lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
@@ -31,6 +31,15 @@ def test_reference_arm_json_line(workload):
     assert d["cpu_baseline"]["kind"] == "port" and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
     assert ("configs[%d]" % {"config2": 1, "config4": 3, "config5": 4}[workload]) in d["config"]["workload"]
+    # the reference arm's config object is the one our arm prints for the workload
+    import bench
+
+    n = {"config2": 1 << 28, "config4": 1 << 30, "config5": 1 << 26}[workload]
+    assert d["config"] == bench.wl_config(workload, n)
+    if workload == "config2":  # the default run carries every other BASELINE config
+        assert sorted(d["workloads"]) == ["config1", "config3", "config4", "config5"]
+        for wl, rec in d["workloads"].items():
+            assert rec["value"] > 0 and rec["config"] == bench.wl_config(wl, bench.WL[wl]["n"])
 
 
 def test_reference_arm_non_zero_ranks_exit_quietly():
@@ -45,24 +54,27 @@ def test_reference_arm_non_zero_ranks_exit_quietly():
     assert r.returncode == 0 and r.stdout.strip() == ""
 
 
-def test_exact_check_of_a_generated_dot(oracle):
-    # the config-4 full-size check on a small instance: the calibrated generator
-    # hits the requested condition and the canonical-order twofold is in bound
+def test_exact_check_of_a_generated_problem(oracle):
+    # the config-4 full-size check on a small instance: the blocked generator
+    # hits the requested condition and the canonical-order twofolds are in bound
     import numpy as np
 
     sys.path.insert(0, str(ROOT))
     import bench
-    from paper_1401_6235_b200 import _lib
+    from paper_1401_6235_b200 import workloads as W
 
-    n = 1 << 15
-    x, y = np.empty(n), np.empty(n)
-    assert _lib.lib().tf_gen_dot_host(n, 1e16, 4242, x.ctypes.data, y.ctypes.data) == 0
+    n = 1 << 17
+    x, y, p = np.empty(n), np.empty(n), np.empty(n)
+    W.gen_ill(W.GEN_DOT, x, y)
+    W.gen_ill(W.GEN_SUM, p)
     zd = oracle.reduce("dot", x, y, geometry=(2, 256, 128))
-    zs = oracle.reduce("sum", x, geometry=(2, 256, 128))
-    c = bench.exact_check(x, y, [float(zd[0]), float(zd[1])], [float(zs[0]), float(zs[1])], 2)
+    zs = oracle.reduce("sum", p, geometry=(2, 256, 128))
+    c = bench.exact_check({"vtdot": (x, y), "vtsum": (p,)}, {"vtdot": zd, "vtsum": zs}, 2)
     assert c["vtdot"]["bound_ok"] and c["vtsum"]["bound_ok"]
-    assert 0.5e16 < c["vtdot"]["cond"] < 2e16
-    assert c["vtdot"]["z0_plus_z1_rel_err"] < 1e-10 < c["vtdot"]["z0_rel_err"]
+    assert 0.5e16 < c["vtdot"]["cond"] < 2e16 and 0.5e16 < c["vtsum"]["cond"] < 2e16
+    assert c["vtdot"]["cond1"] == pytest.approx(c["vtdot"]["cond"] / 2)
+    for k in ("vtdot", "vtsum"):
+        assert c[k]["z0_plus_z1_rel_err"] < 1e-14 < c[k]["z0_rel_err"]
 
 
 REQUIRED = ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
@@ -79,7 +91,8 @@ def test_our_arm_json_line_contract(workload):
     elems = {"config2": 1 << 22, "config4": 1 << 23, "config5": 1 << 22}[workload]
     r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--workload", workload,
                         "--elems", str(elems), "--steps", "3", "--warmup", "3",
-                        "--cpu-sample", str(1 << 20), "--e2e-steps", "1"],
+                        "--cpu-sample", str(1 << 20), "--e2e-steps", "1",
+                        "--no-sub-workloads"],
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
@@ -108,7 +121,11 @@ def test_our_arm_json_line_contract(workload):
         chk = d["device_batch"]["check"]
         assert all(v for op, c in chk.items() if op != "how" for v in c.values()), chk
     elif workload == "config4":
-        assert d["device_batch"]["same_bits_as_separate_reductions"] is True
-        assert d["cpu_baseline"]["check"]["vtdot"]["bound_ok"] is True
+        chk = d["check"]
+        assert all(chk["bit_exact_vs_oracle"].values()), chk
+        for k in ("vtdot", "vtsum"):
+            assert chk["exact"][k]["bound_ok"] is True
+            assert 0.5e16 < chk["exact"][k]["cond"] < 2e16
+        assert all(chk["golden_bits_equal"].values()), chk
     else:
         assert d["check"]["flag_rate"] > 0.99

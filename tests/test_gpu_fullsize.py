@@ -2,8 +2,9 @@
 
 Every element of every output plane is compared bit-exactly with the oracle:
 config 2 (f64 x5 ops, n=2^28), config 3 (f32 x3 ops, n=2^30), config 4 (dot and
-sum, n=2^30, ill-conditioned: bit-exact in the canonical order and inside the
-4u·Σ|terms| bound against the exact accumulator) and config 5 (Horner, 2^26
+sum of its own plane, n=2^30, cond 1e16: bit-exact in the canonical order —
+against the live oracle and the committed golden — and inside the 4u·Σ|terms|
+bound against the exact accumulator) and config 5 (Horner, 2^26
 points, plus the cancellation flag).  Inputs are the bench's own device-
 generated planes (paper_1401_6235_b200.workloads), copied to the host.
 """
@@ -66,31 +67,36 @@ def test_config1_bit_exact(oracle):
 
 
 def test_config4_full_size_dot_and_sum(oracle):
-    from paper_1401_6235_b200 import _lib
+    # BASELINE configs[3] as stated: the dot x.y AND the sum of its own plane p,
+    # n = 2^30, cond ~1e16, half the terms with random exponents in [-50, 50]
+    # (blocked ORO-style generator, run on the device as the bench does)
+    import json
+
+    from conftest import GOLDEN
     from paper_1401_6235_b200 import reduce as R
+    from paper_1401_6235_b200 import workloads as W
 
     n = 1 << 30
-    x = np.empty(n)
-    y = np.empty(n)
-    assert _lib.lib().tf_gen_dot_host(n, 1e16, 4242, x.ctypes.data, y.ctypes.data) == 0
-    X, Y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    X, Y, P = W.config4_planes(n, 0, n, "cuda")
+    zd, zs = R.vtdot(X, Y), R.vtsum(P)
+    x, y, p = _host(X), _host(Y), _host(P)
+    del X, Y, P
     geom = R.geometry(np.float64)
-    z = R.vtdot(X, Y)
-    w = oracle.reduce("dot", x, y, geometry=geom)
-    assert (z.value, z.error) == (float(w[0]), float(w[1]))
-    ok, err, s, t = oracle.bound_ok(z.value, z.error, "dot", x, y)
-    assert ok, (float(err), float(t))
-    cond = float(2 * t / abs(s))
-    assert 0.5e16 < cond < 2e16, cond  # BASELINE's cond ~1e16, at full size
-    # plain double dot in the same order is far off; the twofold is not
-    rel_plain = abs(float(z.value) - float(s)) / abs(float(s))
-    rel_tf = float(err / abs(s))
-    assert rel_tf < 1e-10 and rel_tf < rel_plain
-    zs = R.vtsum(X)
-    ws = oracle.reduce("sum", x, geometry=geom)
-    assert (zs.value, zs.error) == (float(ws[0]), float(ws[1]))
-    ok, err, s2, t2 = oracle.bound_ok(zs.value, zs.error, "sum", x)
-    assert ok
+    golden = json.loads((GOLDEN / "config4.json").read_text())["prefixes"][str(n)]
+    for name, z, rop, planes in (("vtdot", zd, "dot", (x, y)), ("vtsum", zs, "sum", (p,))):
+        # bit-exact against the oracle's canonical order, live and as committed
+        w = oracle.reduce(rop, *planes, geometry=geom)
+        assert (z.value, z.error) == (float(w[0]), float(w[1])), name
+        assert [z.value.hex(), z.error.hex()] == [golden[name]["z0"], golden[name]["z1"]], name
+        # inside 4u * sum|terms| of the exact accumulator, at the stated condition
+        ok, err, s, t = oracle.bound_ok(z.value, z.error, rop, *planes)
+        assert ok, (name, float(err), float(t))
+        cond = float((2 if rop == "dot" else 1) * t / abs(s))
+        assert 0.5e16 < cond < 2e16, (name, cond)
+        # the plain result in the same order is far off; the twofold is not
+        rel_plain = abs(z.value - float(s)) / abs(float(s))
+        rel_tf = float(err / abs(s))
+        assert rel_tf < 1e-14 < rel_plain, (name, rel_tf, rel_plain)
 
 
 def test_config5_full_size_horner(oracle):
