@@ -118,8 +118,13 @@ def test_our_arm_json_line_contract(workload):
     for k in ("sm_mhz", "sm_max_mhz", "reasons"):
         assert k in d["clocks"], k
     if workload == "config2":
-        chk = d["device_batch"]["check"]
-        assert all(v for op, c in chk.items() if op != "how" for v in c.values()), chk
+        chk = d["check"]
+        ops = d["config"]["ops"]
+        assert all(v for op in ops for v in chk[op].values()), chk
+        assert all(chk["oracle_sample"]["bit_exact_vs_oracle"].values()), chk
+        assert chk["batch_equals_per_op_launch_last_op"] is True
+        pg = d["e2e"]["pageable"]
+        assert pg["first_step"] > 0 and pg["steady_state"] > 0
     elif workload == "config4":
         chk = d["check"]
         assert all(chk["bit_exact_vs_oracle"].values()), chk
