@@ -811,7 +811,11 @@ def e2e_elementwise(args, ops, ps, n, esz, world, wlname):
         first = max_over_ranks(times[0], world)
         steady = max_over_ranks(statistics.mean(times[3:]), world)
         u = len(ops) * npg
+        locked = sum(1 for a in list(pcache.values()) + [pout.value, pout.error]
+                     if a.ctypes.data in K._REG)
         rec["pageable"] = {"first_step": world * u / first, "steady_state": world * u / steady,
+                           "step_s": times, "planes_page_locked": locked,
+                           "planes": len(pcache) + 2,
                            "unit": "elem-ops/s", "elems_per_op": npg,
                            "h2d_bytes_per_step": sum(len(p) for p in pcalls) * esz * npg,
                            "d2h_bytes_per_step": 2 * esz * npg * len(ops),

@@ -37,6 +37,30 @@ inline int launch_status(const char* where) { return cuda_status(cudaGetLastErro
 // SM count of the current device (cached per device)
 int sm_count();
 
+// ---- programmatic dependent launch (PDL) ----------------------------------------
+// A kernel launched with the programmatic-stream-serialization attribute may be
+// scheduled while its predecessor on the stream is still draining.  pdl_wait()
+// at the very top (before ANY global-memory access) blocks until the predecessor
+// grid has completed and its writes are visible, so the launch is correct
+// whatever the predecessor was (our kernel, a torch kernel, a memcpy); what
+// overlaps is only the dependent grid's launch and CTA scheduling with the
+// predecessor's tail.  pdl_trigger() lets the next PDL launch start early.
+__device__ __forceinline__ void pdl_wait() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void pdl_trigger() {
+#if defined(__CUDA_ARCH__) && __CUDA_ARCH__ >= 900
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// TF_PDL=0 disables the attribute (A/B runs); default on
+bool pdl_enabled();
+// cudaLaunchKernel with the PDL attribute when enabled
+cudaError_t launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                       cudaStream_t stream);
+
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 // ---- streaming memory helpers --------------------------------------------------

@@ -95,6 +95,11 @@ __global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB : 1
   constexpr int U = (VB == 32) ? (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : 2)) : Unroll<NIN>::U;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  // PDL (launched with programmatic stream serialization): nothing touches
+  // global memory before the predecessor grid has completed; then let the next
+  // launch on the stream be scheduled during this grid's tail
+  pdl_wait();
+  pdl_trigger();
 
   // scalar head (common misalignment) — or everything, when nvec == 0
   for (int64_t i = gtid; i < head; i += gstride) scalar_elem<T, OP>(p, i);
@@ -252,7 +257,7 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
   p.out[0] = static_cast<double*>(out[0]);
   p.out[1] = static_cast<double*>(out[1]);
   void* args[] = {&p, &n, &head, &nvec, &reps};
-  cudaError_t e = cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, stream);
+  cudaError_t e = launch_pdl(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, stream);
   return cuda_status(e, "tf_elementwise: launch");
 }
 

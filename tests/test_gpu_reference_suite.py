@@ -43,7 +43,7 @@ def _run(args, timeout):
     env["PYTHONPATH"] = os.pathsep.join([str(ROOT), str(ROOT / "tests"), str(REF)])
     env.setdefault("NUMBA_CACHE_DIR", "/tmp/tf_numba_cache")
     cmd = [sys.executable, "-m", "pytest", "-p", "refsuite_shim", "-c", os.devnull,
-           "--rootdir", str(SUITE), "-q", "-p", "no:cacheprovider"] + args
+           "--rootdir", str(SUITE), "-p", "no:cacheprovider"] + args
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=str(SUITE),
                        env=env)
     tail = (r.stdout + r.stderr)[-4000:]
