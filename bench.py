@@ -92,6 +92,9 @@ def parse(argv=None):
                     help="between timed steps of an L2-sized working set: write a 512 MB "
                          "buffer, then (write-read) read another 512 MB so the flush's own "
                          "dirty lines are written back before, not inside, the next step")
+    ap.add_argument("--serial-graph", action="store_true",
+                    help="small n: capture the step's ops one after another (shared output "
+                         "planes) instead of as parallel graph branches")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pageable", action="store_true", help="skip the pageable-numpy e2e leg")
     ap.add_argument("--no-device-batch", action="store_true",
@@ -495,8 +498,10 @@ def _host_call_args(K, arity, hp, out):
     return (hp[0], out)
 
 
-def elementwise_ops(wlname, n, offset, dev):
-    """Device planes (workloads.PlaneSet, BASELINE distributions) + raw launchers."""
+def elementwise_ops(wlname, n, offset, dev, separate_outputs=False):
+    """Device planes (workloads.PlaneSet, BASELINE distributions) + raw launchers.
+    The ops share one output pair (they run one after another) unless
+    separate_outputs: then each op writes its own planes (independent ops)."""
     import torch
 
     from paper_1401_6235_b200 import kernels as K
@@ -510,10 +515,13 @@ def elementwise_ops(wlname, n, offset, dev):
     ops = []
     for name in wl["names"]:
         planes = ps.planes(name)
+        if separate_outputs and ops:
+            out = K.empty_twofold(n, tdt, device=dev)
         raw = K.KERNELS[name].loop
         args = list(planes) + [out.value, out.error]
         ops.append(Op(name, (lambda raw=raw, args=args: raw(*args)), (len(planes) + 2) * esz * n,
                       n, planes))
+        ops[-1].out = out
     return ops, ps, out
 
 
@@ -534,6 +542,7 @@ def time_steps(args, ops, ws_bytes, world, local, n):
     ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in ops] for _ in range(K)]
     per_op = {}
+    branches = False
     flush = ws_bytes < (384 << 20)
     scrub = L2Flush(args.l2_flush) if flush else None
     if use_graph:
@@ -552,9 +561,28 @@ def time_steps(args, ops, ws_bytes, world, local, n):
             per_op[op.name] = {"ms": sum(ts) / K, "eager": True}
         g = torch.cuda.CUDAGraph()
         cap = torch.cuda.Stream()
+        branches = len(ops) > 1 and len({id(op.out) for op in ops}) == len(ops)
         with torch.cuda.graph(g, stream=cap):
-            for op in ops:
-                op.launch()
+            if branches:
+                # independent ops (own output planes): parallel graph branches, so
+                # one op's ramp and tail overlap the other's
+                fork = torch.cuda.Event()
+                fork.record(cap)
+                joins = []
+                for op in ops[1:]:
+                    st = torch.cuda.Stream()
+                    st.wait_event(fork)
+                    with torch.cuda.stream(st):
+                        op.launch()
+                    j = torch.cuda.Event()
+                    j.record(st)
+                    joins.append(j)
+                ops[0].launch()
+                for j in joins:
+                    cap.wait_event(j)
+            else:
+                for op in ops:
+                    op.launch()
         g.replay()
         torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -594,6 +622,7 @@ def time_steps(args, ops, ws_bytes, world, local, n):
         per_op[op.name] = {"ms": avg, "gbs": op.nbytes / (avg * 1e-3) / 1e9,
                            "bytes": op.nbytes, "share": share}
     return {"elapsed_ms": elapsed_ms, "per_op": per_op, "use_graph": use_graph,
+            "graph_branches": bool(use_graph and branches),
             "flush": scrub.describe() if flush else None, "clocks": clk.summary(),
             "launches": K * len(ops)}
 
@@ -804,12 +833,12 @@ def e2e_elementwise(args, ops, ps, n, esz, world, wlname):
         pc = [_host_call_args(K, K.KERNELS[op.name].arity, pp, pout) for op, pp in zip(ops, pcalls)]
         barrier(world)
         times = []
-        for _ in range(6):
+        for _ in range(8):
             t0 = time.perf_counter()
             per_call_step(pc)
             times.append(time.perf_counter() - t0)
         first = max_over_ranks(times[0], world)
-        steady = max_over_ranks(statistics.mean(times[3:]), world)
+        steady = max_over_ranks(statistics.mean(times[5:]), world)
         u = len(ops) * npg
         locked = sum(1 for a in list(pcache.values()) + [pout.value, pout.error]
                      if a.ctypes.data in K._REG)
@@ -821,7 +850,8 @@ def e2e_elementwise(args, ops, ps, n, esz, world, wlname):
                            "d2h_bytes_per_step": 2 * esz * npg * len(ops),
                            "path": "kernels.<op>(plain numpy planes) per op: staged through "
                                    "pinned buffers; planes reused 4 times get page-locked "
-                                   "(steady state = mean of steps 4-6)"}
+                                   "(a plane read once per step locks during step 4; "
+                                   "steady state = mean of steps 6-8)"}
         del pcache, pcalls, pout, pc
     return rec
 
@@ -887,7 +917,9 @@ def run_elementwise(args, rank, world, local, wlname):
         lo, hi = rank * n_cfg, (rank + 1) * n_cfg
     n = hi - lo
     log("%s: generating inputs n=%d (%s)" % (wlname, n, args.scaling))
-    ops, ps, out = elementwise_ops(wlname, n, lo, torch.cuda.current_device())
+    small = args.graph == "on" or (args.graph == "auto" and n <= (1 << 22))
+    ops, ps, out = elementwise_ops(wlname, n, lo, torch.cuda.current_device(),
+                                   separate_outputs=small and not args.serial_graph)
     torch.cuda.synchronize()
     ws_bytes = sum(t.numel() * t.element_size() for t in ps.cache.values()) + 2 * n * esz
     tm = time_steps(args, ops, ws_bytes, world, local, n)
@@ -907,10 +939,13 @@ def run_elementwise(args, rank, world, local, wlname):
         check = ieee_check(ops, bouts)
         if rank == 0:
             check["oracle_sample"] = oracle_sample_check(ops, bouts)
-            # the batch's bits equal one launch per op (the headline path): the
-            # last timed op's output vs the batch's for that op
-            check["batch_equals_per_op_launch_last_op"] = bool(
-                torch.equal(bouts[-1].value, out.value) and torch.equal(bouts[-1].error, out.error))
+            # the batch's bits equal one launch per op (the headline path): every
+            # op whose output planes no later op overwrote, vs the batch's for it
+            last = {id(op.out): j for j, op in enumerate(ops)}
+            check["batch_equals_per_op_launch"] = {
+                ops[j].name: bool(torch.equal(bouts[j].value, ops[j].out.value)
+                                  and torch.equal(bouts[j].error, ops[j].out.error))
+                for j in sorted(last.values())}
         del bouts
     e2e = None
     if not args.no_e2e:
@@ -953,7 +988,10 @@ def run_elementwise(args, rank, world, local, wlname):
         "data": "synthetic (seeded, device-generated with BASELINE distributions)",
         "config": wl_config(wlname, n_cfg, args.scaling),
         "config_detail": {
-            "timing": "cuda-graph replay per step" if tm["use_graph"] else "eager launches",
+            "timing": ("cuda-graph replay per step" + (
+                "; the ops are independent (each its own output planes) and run as parallel "
+                "graph branches" if tm["graph_branches"] else "")) if tm["use_graph"]
+            else "eager launches",
             "l2_flush": tm["flush"], "layout": "split SoA planes",
             "inputs": "tf_fill counter-based splitmix64 on the device; plane k seed 1000+17k, "
                       "element i of a rank is global index lo+i",
@@ -1178,17 +1216,17 @@ def run_config4(args, rank, world, local):
             npg = min(ne, PAGEABLE_MAX)
             xp, yp, pp = (np.array(a[:npg], copy=True) for a in (xh, yh, ph))
             times = []
-            for _ in range(6):
+            for _ in range(8):
                 t0 = time.perf_counter()
                 R.vtdot(xp, yp)
                 R.vtsum(pp)
                 times.append(time.perf_counter() - t0)
             e2e["pageable"] = {"first_step": world * 2 * npg / max_over_ranks(times[0], world),
                                "steady_state": world * 2 * npg /
-                               max_over_ranks(statistics.mean(times[3:]), world),
+                               max_over_ranks(statistics.mean(times[5:]), world),
                                "unit": "elem-ops/s", "elems_per_step": npg,
                                "path": "reduce.vtdot / vtsum on plain numpy planes (staged; "
-                                       "page-locked after 4 uses)"}
+                                       "page-locked after 4 uses; steady = steps 6-8)"}
             del xp, yp, pp
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -1421,15 +1459,16 @@ def run_config5(args, rank, world, local):
             xp = np.array(xh[:npg], copy=True)
             op_ = Kmod.empty_twofold(npg)  # numpy planes (the reference's default)
             times = []
-            for _ in range(6):
+            for _ in range(8):
                 t0 = time.perf_counter()
                 R.vthorner(c, xp, op_)
                 times.append(time.perf_counter() - t0)
             e2e["pageable"] = {"first_step": world * npg / max_over_ranks(times[0], world),
                                "steady_state": world * npg /
-                               max_over_ranks(statistics.mean(times[3:]), world),
+                               max_over_ranks(statistics.mean(times[5:]), world),
                                "unit": "points/s", "elems_per_step": npg,
-                               "path": "reduce.vthorner on plain numpy planes"}
+                               "path": "reduce.vthorner on plain numpy planes (staged; "
+                                       "page-locked after 4 uses; steady = steps 6-8)"}
             del xp, op_
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -122,7 +122,7 @@ def test_our_arm_json_line_contract(workload):
         ops = d["config"]["ops"]
         assert all(v for op in ops for v in chk[op].values()), chk
         assert all(chk["oracle_sample"]["bit_exact_vs_oracle"].values()), chk
-        assert chk["batch_equals_per_op_launch_last_op"] is True
+        assert chk["batch_equals_per_op_launch"] and all(chk["batch_equals_per_op_launch"].values())
         pg = d["e2e"]["pageable"]
         assert pg["first_step"] > 0 and pg["steady_state"] > 0
     elif workload == "config4":
