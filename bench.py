@@ -359,8 +359,14 @@ class L2Flush:
                 else "512 MB memset between steps") + " (outside the timed intervals)"
 
 
-def _best_of(fn, reps=3):
-    fn()  # warm-up (thread pool, page faults)
+def _best_of(fn, reps=3, warm_s=1.0):
+    # warm up for ~1 s (thread pool, page faults, and the host CPUs' clocks: on
+    # the GPU boxes a cold first second of OpenMP work ran ~1.7x slower,
+    # profiles/r2_cpu_probe.json)
+    t0 = time.perf_counter()
+    fn()
+    while time.perf_counter() - t0 < warm_s:
+        fn()
     best = None
     for _ in range(reps):
         t0 = time.perf_counter()
