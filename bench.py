@@ -1551,9 +1551,12 @@ def _reference_line(args, wlname, metric, value, unit, dtype, n_cfg, sample, nt,
     return line
 
 
-def _timed_steps(steps, warmup, step):
-    for _ in range(max(warmup, 1)):
+def _timed_steps(steps, warmup, step, warm_s=1.0):
+    t0 = time.perf_counter()
+    k = 0
+    while k < max(warmup, 1) or time.perf_counter() - t0 < warm_s:  # also warms the CPUs
         step()
+        k += 1
     t0 = time.perf_counter()
     for _ in range(steps):
         step()
