@@ -25,6 +25,7 @@ from __future__ import annotations
 import argparse
 import csv
 import json
+import re
 import zlib
 from dataclasses import dataclass
 from pathlib import Path
@@ -73,53 +74,61 @@ class BenchRecord:
     ops_per_elem: int = 0
 
 
+def _selection(kind, given, known, hint=""):
+    """The reference harness's selection rule (bench.py:184-199): None means every
+    known entry; an unknown name is a ValueError naming it."""
+    picked = list(known) if given is None else list(given)
+    bad = [x for x in picked if x not in known]
+    if bad:
+        raise ValueError("unknown %s %r%s" % (kind, bad[0], hint))
+    return picked
+
+
 def make_plan(ops=None, formats=None, sizes=None):
-    """Expand op/format/size selections into plan cells (bench.py:184-199)."""
-    ops = list(KERNELS) if ops is None else list(ops)
-    formats = list(_FORMATS) if formats is None else list(formats)
-    sizes = list(SIZES) if sizes is None else list(sizes)
-    for op in ops:
-        if op not in KERNELS:
-            raise ValueError("unknown op %r" % op)
+    """Plan cells (op, arity, format, size class), format-major then size then op —
+    the reference's cell order (bench.py:184-199)."""
+    ops = _selection("op", ops, KERNELS)
+    formats = _selection("format", formats, _FORMATS, " (use f32/f64)")
+    sizes = _selection("size class", sizes, SIZES)
+    cells = []
     for fmt in formats:
-        if fmt not in _FORMATS:
-            raise ValueError("unknown format %r (use f32/f64)" % fmt)
-    for size in sizes:
-        if size not in SIZES:
-            raise ValueError("unknown size class %r" % size)
-    return [(op, KERNELS[op].arity, fmt, size)
-            for fmt in formats for size in sizes for op in ops]
+        for size in sizes:
+            cells.extend((op, KERNELS[op].arity, fmt, size) for op in ops)
+    return cells
 
 
-def _seed(op, fmt, n):
-    return zlib.crc32(("%s:%s:%d" % (op, fmt, n)).encode())
+def _cell_seed(op, fmt, n):
+    # the reference's per-cell seed (bench.py:144-145): crc32 of "op:fmt:n"
+    return zlib.crc32(f"{op}:{fmt}:{n}".encode())
 
 
-def _planes(rng, n, dtype, positive=False):
-    v = rng.uniform(1.0, 2.0, n)
-    if not positive:
-        v *= rng.choice((-1.0, 1.0), n)
+def _value_and_tail(gen, n, dtype, signed=True):
+    """Magnitudes in [1, 2) (random sign unless `signed` is False) and a tail
+    2^-54 (f64) / 2^-25 (f32) below each, drawn in the reference's order
+    (bench.py:148-153) so the planes match its inputs value for value."""
+    v = gen.uniform(1.0, 2.0, n)
+    if signed:
+        v *= gen.choice((-1.0, 1.0), n)
     v = v.astype(dtype)
-    scale = dtype(2.0 ** -54) if dtype is np.float64 else dtype(2.0 ** -25)
-    return v, (v * scale).astype(dtype)
+    tail_scale = dtype(2.0 ** -54) if dtype is np.float64 else dtype(2.0 ** -25)
+    return v, (v * tail_scale).astype(dtype)
+
+
+# planes of x and of y each arity takes: (x value[, x error]), (y value[, y error])
+_TAKE = {"22": (2, 2), "21": (2, 1), "11": (1, 1), "u2": (2, 0), "u1": (1, 0)}
 
 
 def inputs(op, fmt, n):
-    """Deterministic, well-scaled argument planes for one cell (host numpy)."""
+    """Seeded host planes for one cell, the same values the reference harness
+    feeds its loops (bench.py:156-162)."""
     spec = KERNELS[op]
     dtype = _FORMATS[fmt]
-    rng = np.random.default_rng(_seed(op, fmt, n))
-    xv, xe = _planes(rng, n, dtype, spec.baseline == "sqrt")
-    if spec.arity == "22":
-        yv, ye = _planes(rng, n, dtype)
-        return (xv, xe, yv, ye)
-    if spec.arity == "21":
-        return (xv, xe, _planes(rng, n, dtype)[0])
-    if spec.arity == "11":
-        return (xv, _planes(rng, n, dtype)[0])
-    if spec.arity == "u2":
-        return (xv, xe)
-    return (xv,)
+    gen = np.random.default_rng(_cell_seed(op, fmt, n))
+    nx, ny = _TAKE[spec.arity]
+    planes = list(_value_and_tail(gen, n, dtype, signed=spec.baseline != "sqrt"))[:nx]
+    if ny:
+        planes += list(_value_and_tail(gen, n, dtype))[:ny]
+    return tuple(planes)
 
 
 def _measure(launch, repetitions, min_s=0.010, max_iters=1 << 14):
@@ -221,10 +230,10 @@ def run_bench(plan=None, repetitions=5, device=0, layout="split"):
         tdt = torch.float64 if dtype is np.float64 else torch.float32
         dt = _lib.TF_F64 if dtype is np.float64 else _lib.TF_F32
         for name in ("vadd", "vmul", "vdiv", "vsqrt", "vmem"):
-            rng = np.random.default_rng(_seed(name, fmt, n))
-            x = torch.from_numpy(_planes(rng, n, dtype, name == "vsqrt")[0]).cuda()
+            gen = np.random.default_rng(_cell_seed(name, fmt, n))
+            x = torch.from_numpy(_value_and_tail(gen, n, dtype, name != "vsqrt")[0]).cuda()
             unary = name in ("vsqrt", "vmem")
-            y = None if unary else torch.from_numpy(_planes(rng, n, dtype)[0]).cuda()
+            y = None if unary else torch.from_numpy(_value_and_tail(gen, n, dtype)[0]).cuda()
             r = torch.empty(n, dtype=tdt, device="cuda")
             iters, best = _measure(_dotted_launcher(name, dt, n, x, y, r), repetitions)
             mega = n * iters / best / 1e6
@@ -256,31 +265,43 @@ def run_bench(plan=None, repetitions=5, device=0, layout="split"):
     return records
 
 
-CSV_HEADER = ["op", "shape", "format", "size_class", "elements", "mega_ops", "ratio_vs_dotted",
-              "gpus", "gbps", "roofline_frac", "bytes_per_elem", "ops_per_elem"]
+# (column, CSV format, table header, table format); the first seven are the
+# reference's stable CSV layout (bench.py:270-279), the rest are GPU columns
+_COLUMNS = [
+    ("op", "%s", "op", "%-8s"), ("shape", "%s", "shape", "%-5s"),
+    ("format", "%s", "fmt", "%-4s"), ("size_class", "%s", "size", "%-6s"),
+    ("elements", "%d", "elements", "%10d"), ("mega_ops", "%.3f", "mega_ops", "%12.1f"),
+    ("ratio_vs_dotted", "%.4f", "ratio", "%8.2f"), ("gpus", "%d", None, None),
+    ("gbps", "%.1f", "GB/s", "%9.1f"), ("roofline_frac", "%.4f", "roof", "%7.3f"),
+    ("bytes_per_elem", "%d", None, None), ("ops_per_elem", "%d", None, None),
+]
+CSV_HEADER = [c[0] for c in _COLUMNS]
 
 
 def write_csv(records, path):
-    """The reference's stable CSV layout (bench.py:270-279) + GPU columns."""
+    """Records as CSV: the reference's columns, then the GPU columns.  A missing
+    ratio (vmem has no dotted baseline) is an empty field."""
     with open(path, "w", newline="") as fh:
         w = csv.writer(fh)
         w.writerow(CSV_HEADER)
         for r in records:
-            ratio = "" if r.ratio_vs_dotted is None else "%.4f" % r.ratio_vs_dotted
-            w.writerow([r.op, r.shape, r.format, r.size_class, r.elements, "%.3f" % r.mega_ops,
-                        ratio, r.gpus, "%.1f" % r.gbps, "%.4f" % r.roofline_frac,
-                        r.bytes_per_elem, r.ops_per_elem])
+            w.writerow(["" if getattr(r, name) is None else fmt % getattr(r, name)
+                        for name, fmt, _, _ in _COLUMNS])
 
 
 def format_table(records) -> str:
-    lines = ["%-8s %-5s %-4s %-6s %10s %12s %8s %9s %7s"
-             % ("op", "shape", "fmt", "size", "elements", "mega_ops", "ratio", "GB/s", "roof")]
+    """Fixed-width table of the records, in the order they arrive."""
+    cols = [(name, head, fmt) for name, _, head, fmt in _COLUMNS if head]
+    width = lambda fmt: int(re.match(r"%-?(\d+)", fmt).group(1))  # noqa: E731
+    out = [" ".join(head.ljust(width(fmt)) if fmt.startswith("%-") else head.rjust(width(fmt))
+                    for _, head, fmt in cols)]
     for r in records:
-        ratio = "-" if r.ratio_vs_dotted is None else "%8.2f" % r.ratio_vs_dotted
-        lines.append("%-8s %-5s %-4s %-6s %10d %12.1f %8s %9.1f %7.3f"
-                     % (r.op, r.shape, r.format, r.size_class, r.elements, r.mega_ops, ratio,
-                        r.gbps, r.roofline_frac))
-    return "\n".join(lines) + "\n"
+        cells = []
+        for name, _, fmt in cols:
+            v = getattr(r, name)
+            cells.append("-".rjust(width(fmt)) if v is None else fmt % v)
+        out.append(" ".join(cells))
+    return "\n".join(out) + "\n"
 
 
 def main(argv=None):
