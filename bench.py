@@ -111,6 +111,9 @@ def parse(argv=None):
                     help="elements of each sub-workload (default: the config's; dry runs)")
     ap.add_argument("--cpu-sample", type=int, default=1 << 26,
                     help="elements per op in the CPU baseline sample")
+    ap.add_argument("--no-numba-ref", action="store_true",
+                    help="reference arm: skip timing the numba reference package itself "
+                         "(then the arm is the C port alone)")
     ap.add_argument("--ref-elems", type=int, default=0,
                     help="reference arm: elements per op per step (default: the config's "
                          "full size where host RAM allows, else a bounded sample)")
@@ -1585,11 +1588,121 @@ def reference_elementwise(args, wlname, steps):
     sample = ("%s %d elements per op x %d ops per step, oracle/twofold_oracle.c (OpenMP, -O3 "
               "-march=x86-64-v3, no contraction)"
               % ("all" if ns == n_cfg else "a sample of", ns, len(wl["names"])))
-    del inputs, out
-    return _reference_line(args, wlname, METRIC if wlname == "config2" else METRIC + " [%s]" % wlname,
+    del out
+    port = {"value": value, "cores": nt, "sample": sample, "ms_per_step": 1e3 * dt / steps}
+    numba = None
+    if not args.no_numba_ref:
+        gc.collect()
+        try:
+            numba = _numba_reference_timing(wlname, inputs, ns, steps, args.warmup)
+        except Exception as e:  # noqa: BLE001
+            numba = {"unavailable": "%s: %s" % (type(e).__name__, e)}
+    del inputs
+    # the arm's value is the STRONGER of the two CPU implementations on this box:
+    # the reference package itself (numba, fork-sharded) or the 16-thread C port
+    kind = "port"
+    if numba and "value" in numba and numba["value"] > value:
+        kind, value, nt = "reference", numba["value"], numba["cores"]
+        sample = numba["sample"] + ", " + numba["code"]
+    line = _reference_line(args, wlname, METRIC if wlname == "config2" else METRIC + " [%s]" % wlname,
                            value, "elem-ops/s",
                            "f64" if wl["dtype"] == np.float64 else "f32", n_cfg, sample, nt,
-                           steps, 1e3 * dt / steps, sample_elems_per_op=ns)
+                           steps, 1e3 * len(wl["names"]) * ns / value, sample_elems_per_op=ns,
+                           port=port, numba_reference=numba)
+    line["cpu_baseline"]["kind"] = kind
+    return line
+
+
+def _numba_reference_timing(wlname, inputs, ns, steps, warmup):
+    """The reference package itself (twofold.kernels, numba, staged unmodified in
+    baseline/_ref) on the same planes as the port leg, as BASELINE.md §5 plans it:
+    KERNELS[name].func on numpy planes, fork-sharded over all host cores in
+    contiguous slices (the numba loops hold the GIL, so threads do not scale),
+    warm-up steps first (numba compile, page faults), then `steps` timed steps of
+    every op between two barriers; throughput = elements / slowest process.  P = 1
+    is timed too (one step).  None when the staged package or numba is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "twofold").is_dir():
+        return None
+    try:
+        import multiprocessing as mp
+
+        os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tf_numba_cache")
+        sys.path.insert(0, str(ref))
+        import twofold.kernels as RK  # the reference's own module
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": "%s: %s" % (type(e).__name__, e)}
+    finally:
+        if sys.path and sys.path[0] == str(ref):
+            sys.path.pop(0)
+    wl = WL[wlname]
+
+    def step(lo, hi, out):
+        for name in wl["names"]:
+            spec = RK.KERNELS[name]
+            pl = [q[lo:hi] for q in inputs[name]]
+            if spec.arity == "22":
+                spec.func(RK.TwofoldArray(pl[0], pl[1]), RK.TwofoldArray(pl[2], pl[3]), out)
+            elif spec.arity == "21":
+                spec.func(RK.TwofoldArray(pl[0], pl[1]), pl[2], out)
+            elif spec.arity == "u2":
+                spec.func(RK.TwofoldArray(pl[0], pl[1]), out)
+            else:
+                spec.func(*pl, out)
+
+    n1 = min(ns, 1 << 24)  # the single-process figure on a bounded sample
+    out1 = RK.empty_twofold(n1, wl["dtype"])
+    step(0, n1, out1)  # compile
+    t0 = time.perf_counter()
+    step(0, n1, out1)
+    t1 = time.perf_counter() - t0
+    del out1
+    p = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    bar = ctx.Barrier(p + 1)
+    q = ctx.Queue()
+
+    def child(r):
+        lo, hi = ns * r // p, ns * (r + 1) // p
+        out = RK.empty_twofold(hi - lo, wl["dtype"])
+        for _ in range(max(1, warmup)):
+            step(lo, hi, out)
+        bar.wait()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            step(lo, hi, out)
+        q.put(time.perf_counter() - t0)
+        bar.wait()
+
+    procs = [ctx.Process(target=child, args=(r,)) for r in range(p)]
+    for pr in procs:
+        pr.start()
+    bar.wait()
+    bar.wait()
+    tp = max(q.get() for _ in procs)
+    for pr in procs:
+        pr.join()
+    nops = len(wl["names"])
+    return {"value": nops * ns * steps / tp, "unit": "elem-ops/s", "cores": p,
+            "sample": "%d elements per op x %d ops per step (%s), %d steps after %d warm-up, "
+                      "the port leg's planes" % (ns, nops, "/".join(wl["names"]), steps,
+                                                 max(1, warmup), ),
+            "how": "fork-sharded contiguous slices over all host cores, barrier before and "
+                   "after the timed steps, elements / slowest process",
+            "single_process": {"value": nops * n1 / t1, "cores": 1, "steps": 1,
+                               "elems_per_op": n1},
+            "code": "baseline/_ref/twofold/kernels.py KERNELS[name].func (numba %s)"
+                    % _numba_version()}
+
+
+def _numba_version():
+    try:
+        import numba
+
+        return numba.__version__
+    except Exception:  # noqa: BLE001
+        return "?"
+
 
 
 def reference_config4(args, steps):

@@ -71,6 +71,7 @@ def _bind(L: ctypes.CDLL) -> None:
         "tf_fill": (ci, [ci, ci, i64, ctypes.c_uint64, i64, cd, cd, vp, vp, vp]),
         "tf_dotted": (ci, [ci, ci, i64, vp, vp, vp, vp]),
         "tf_fp64_peak": (ci, [ci, ctypes.POINTER(cd), ctypes.POINTER(cd)]),
+        "tf_fastpath_check": (ci, [ci, i64, ctypes.c_uint64, ctypes.POINTER(i64)]),
         "tf_gen_dot_host": (ci, [i64, cd, ctypes.c_uint64, vp, vp]),
         "tf_gen_ill": (ci, [ci, i64, i64, i64, cd, ctypes.c_uint64, ci, ci, vp, vp, vp]),
         "tf_gen_ill_host": (ci, [ci, i64, i64, i64, cd, ctypes.c_uint64, ci, ci, vp, vp, ci]),
@@ -87,7 +88,7 @@ EXPORTS = (
     "tf_reduce_geometry", "tf_reduce_workspace_bytes", "tf_reduce", "tf_reduce_pair",
     "tf_combine", "tf_reduce_host", "tf_reduce_host_batch", "tf_xgpu_mailbox", "tf_xgpu_open", "tf_xgpu_combine",
     "tf_xgpu_status", "tf_xgpu_emulate", "tf_xgpu_reduce", "tf_xgpu_reduce_emulate",
-    "tf_xgpu_publish", "tf_xgpu_reduce_publish", "tf_xgpu_collect", "tf_horner", "tf_horner_host", "tf_fill", "tf_dotted", "tf_fp64_peak", "tf_gen_dot_host",
+    "tf_xgpu_publish", "tf_xgpu_reduce_publish", "tf_xgpu_collect", "tf_horner", "tf_horner_host", "tf_fill", "tf_dotted", "tf_fp64_peak", "tf_fastpath_check", "tf_gen_dot_host",
     "tf_gen_ill", "tf_gen_ill_host",
 )
 

@@ -59,20 +59,11 @@ template <class T, int OP>
 __device__ __forceinline__ void batch_vec(const BatchOp<T>& b, int64_t head, int64_t j) {
   constexpr int NIN = OpInfo<OP>::NIN;
   using V = Vec32<T>;
-  constexpr int E = V::N;
   V r[NIN];
 #pragma unroll
   for (int k = 0; k < NIN; k++) r[k] = ld_keep(reinterpret_cast<const V*>(b.in[k] + head) + j);
   V o0, o1;
-#pragma unroll
-  for (int e = 0; e < E; e++) {
-    T v[NIN];
-#pragma unroll
-    for (int k = 0; k < NIN; k++) v[k] = r[k].v[e];
-    P<T> z = apply<T, OP>(v);
-    o0.v[e] = z.a;
-    o1.v[e] = z.b;
-  }
+  apply_vec<T, OP, V, false>(r, o0, o1);  // intrinsics: fewer registers (A/B r2)
   st_stream(reinterpret_cast<V*>(b.out[0] + head) + j, o0);
   st_stream(reinterpret_cast<V*>(b.out[1] + head) + j, o1);
 }

@@ -36,6 +36,17 @@
 #define TF_SQRT_U 1
 #endif
 
+// shared-memory stages of the TMA-staged variant, by input-plane count (A/B builds)
+#ifndef TF_BULK_NST2
+#define TF_BULK_NST2 3
+#endif
+#ifndef TF_BULK_NST3
+#define TF_BULK_NST3 3
+#endif
+#ifndef TF_BULK_NST4
+#define TF_BULK_NST4 2
+#endif
+
 namespace tf {
 
 template <class T>
@@ -60,26 +71,27 @@ __device__ __forceinline__ void scalar_elem(const Planes<T>& p, int64_t i) {
   st_stream(p.out[1] + i, z.b);
 }
 
+// The register path takes the branch-free f64 fast paths (tf_math.cuh
+// div_fast/sqrt_fast, all lanes of a vector interleaved) only where that beat the
+// intrinsics at the hbm size (profiles/r2_fastpath_ab.txt): vtdiv and vtsqrt,
+// +12% and +6%.  For vtdiv2 and vtsqrt1 the interleaved lanes raise registers
+// past four resident CTAs per SM and cost more bytes in flight than the ILP
+// gains; those run on the TMA-staged path (ew_bulk_kernel) instead.
+template <int OP>
+__host__ __device__ constexpr bool reg_fast_op() {
+  return OP == 11 || OP == 13;
+}
+
 template <class T, int OP, int VB, int U>
 __device__ __forceinline__ void compute_store(const VecN<T, VB> (&r)[U][OpInfo<OP>::NIN],
                                               int64_t base, int64_t nvec, VecN<T, VB>* vo0,
                                               VecN<T, VB>* vo1) {
-  constexpr int NIN = OpInfo<OP>::NIN;
-  constexpr int E = VecN<T, VB>::N;
 #pragma unroll
   for (int u = 0; u < U; u++) {
     const int64_t j = base + u * 256;
     if (j < nvec) {
       VecN<T, VB> o0, o1;
-#pragma unroll
-      for (int e = 0; e < E; e++) {
-        T v[NIN];
-#pragma unroll
-        for (int k = 0; k < NIN; k++) v[k] = r[u][k].v[e];
-        P<T> z = apply<T, OP>(v);
-        o0.v[e] = z.a;
-        o1.v[e] = z.b;
-      }
+      apply_vec<T, OP, VecN<T, VB>, reg_fast_op<OP>()>(r[u], o0, o1);
       st_stream(vo0 + j, o0);
       st_stream(vo1 + j, o1);
     }
@@ -138,6 +150,96 @@ __global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB : 1
   }
 }
 
+// ---- TMA-staged variant: bulk async copies into a shared-memory ring ------------
+// Inputs arrive through cp.async.bulk (the TMA engine's UBLKCP) into NST stages of
+// one 256-vector tile (8 KB) per input plane.  Each thread reads its 32-byte
+// vectors from shared memory, computes and stores; then the CTA syncs and one
+// thread refills the slot with the tile NST ahead — so NST-1 tiles per CTA stay
+// in flight while every warp computes, bounded by shared memory instead of
+// registers.  That is what vtsqrt1 lacks on the register
+// path: two IEEE square roots and a division per element (~41 FP64 instructions)
+// leave warps computing, not loading, for most of their time.  Outputs leave as
+// 256-bit streaming stores straight from registers.  One CTA per chunk of `reps`
+// tiles (the hardware block scheduler balances the SMs); scalar head and tail as
+// in ew_kernel.  Same per-element core, so outputs are bit-identical to it.
+template <class T, int OP>
+struct BulkEw {
+  static constexpr int NIN = OpInfo<OP>::NIN;
+  static constexpr int TILE = 256 * 32;  // bytes per plane per tile
+  static constexpr int NST = NIN <= 2 ? TF_BULK_NST2 : (NIN == 3 ? TF_BULK_NST3 : TF_BULK_NST4);
+  static constexpr int SMEM = NST * NIN * TILE;  // 32 KB (2 planes) .. 64 KB (4 planes)
+};
+
+template <class T, int OP>
+__global__ void __launch_bounds__(256) ew_bulk_kernel(Planes<T> p, int64_t n, int64_t head,
+                                                      int64_t nvec, int reps) {
+  using B = BulkEw<T, OP>;
+  constexpr int NIN = B::NIN;
+  using V = Vec32<T>;
+  constexpr int E = V::N;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bar[B::NST];
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = gtid; i < head; i += gstride) scalar_elem<T, OP>(p, i);
+  const int64_t tail0 = head + nvec * E;
+  for (int64_t i = tail0 + gtid; i < n; i += gstride) scalar_elem<T, OP>(p, i);
+
+  const int64_t ntile = (nvec + 255) / 256;
+  const int64_t t0 = (int64_t)blockIdx.x * reps;
+  if (t0 >= ntile) return;
+  const int cnt = (int)(ntile - t0 < reps ? ntile - t0 : reps);
+  const T* src[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; k++) src[k] = p.in[k] + head;
+  V* vo0 = reinterpret_cast<V*>(p.out[0] + head);
+  V* vo1 = reinterpret_cast<V*>(p.out[1] + head);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int q = 0; q < B::NST; q++) mbar_init(&bar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int j, int buf) {
+    const int64_t v0 = (t0 + j) * 256;
+    const int64_t left = nvec - v0;
+    const uint32_t bytes = (uint32_t)(left < 256 ? left : 256) * 32u;
+    const uint64_t pol = l2_evict_first_policy();
+    mbar_expect_tx(&bar[buf], bytes * NIN);
+#pragma unroll
+    for (int k = 0; k < NIN; k++)
+      bulk_g2s_hint(smem + (buf * NIN + k) * B::TILE, src[k] + v0 * E, bytes, &bar[buf], pol);
+  };
+  if (threadIdx.x == 0)
+    for (int q = 0; q < B::NST && q < cnt; q++) issue(q, q);
+#pragma unroll 1
+  for (int j = 0; j < cnt; j++) {
+    const int buf = j % B::NST;
+    mbar_wait(&bar[buf], (uint32_t)((j / B::NST) & 1));
+    const int64_t jv = (t0 + j) * 256 + threadIdx.x;
+    const bool act = jv < nvec;
+    if (act) {
+      V r[NIN];
+#pragma unroll
+      for (int k = 0; k < NIN; k++)
+        r[k] = *reinterpret_cast<const V*>(smem + (buf * NIN + k) * B::TILE + threadIdx.x * 32);
+      V o0, o1;
+      apply_vec<T, OP>(r, o0, o1);
+      st_stream(vo0 + jv, o0);
+      st_stream(vo1 + jv, o1);
+    }
+    // Refill this slot only after every thread has USED its vectors: the refill
+    // is an async-proxy write into the slot, and bar.sync alone does not wait
+    // for a shared-memory read's data to come back — a read still in flight
+    // when thread 0 issued the copy returned the NEXT tile (seen on vtsqrt1,
+    // tools/bulk_debug.py).  The other NST-1 slots stay in flight meanwhile.
+    __syncthreads();
+    if (threadIdx.x == 0 && j + B::NST < cnt) issue(j + B::NST, buf);
+  }
+}
+
 // ---- dispatch ------------------------------------------------------------------
 
 struct EwEntry {
@@ -146,7 +248,20 @@ struct EwEntry {
   int unroll;
   int reps;  // default chunk length in 256*unroll-vector steps (hbm sweep, profiles)
   std::atomic<int> max_blocks_per_sm;  // occupancy, filled lazily (idempotent)
+  const void* bulk_fn;  // TMA-staged variant (ew_bulk_kernel), 32-byte vectors only
+  int bulk_smem;
+  int bulk_default;  // the bulk variant is the default for this op
+  int bulk_reps;     // tiles per CTA
+  std::atomic<unsigned> bulk_attr_set;  // per-device bit: max dynamic smem raised
 };
+
+// Ops whose TMA-staged variant is the default (f64 ops with an IEEE division or
+// square root per element, A/B-measured on config-2 planes at 2^28:
+// profiles/r2_bulk_ab.txt).  TF_EW_BULK=0 / =all override it.
+template <class T, int OP>
+constexpr bool bulk_default_op() {
+  return sizeof(T) == 8 && (OP == 3 || OP == 12);
+}
 
 template <class T, int OP, int VB>
 EwEntry make_entry() {
@@ -156,7 +271,16 @@ EwEntry make_entry() {
   // for the 48 B/element ops; profiles/r1s2_chunk_reps_hbm.txt), except vtsqrt1
   // (div + 2 sqrt per element, U = 1): four steps (profiles/r2_sqrt_ab.txt)
   constexpr int REPS = OP == 12 ? 4 : 1;
-  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>), NIN, U, REPS, {0}};
+  return EwEntry{reinterpret_cast<const void*>(&ew_kernel<T, OP, VB>),
+                 NIN,
+                 U,
+                 REPS,
+                 {0},
+                 reinterpret_cast<const void*>(&ew_bulk_kernel<T, OP>),
+                 BulkEw<T, OP>::SMEM,
+                 bulk_default_op<T, OP>(),
+                 NIN <= 2 ? 8 : 4,
+                 {0u}};
 }
 
 template <class T, int VB, int... OPS>
@@ -220,6 +344,50 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
   } else {
     head = n;
     nvec = 0;
+  }
+
+  // TMA-staged variant (ew_bulk_kernel): TF_EW_BULK=0 never, =all for every op,
+  // default per op (bulk_default); chunk = TF_EW_BULK_REPS tiles (default 8 for
+// one- and two-plane ops, 4 for three and four planes: profiles/r2_bulk_ab.txt)
+  static const int bulk_mode = [] {  // 0 never, 1 default ops, 2 all ops
+    const char* e = getenv("TF_EW_BULK");
+    if (!e) return 1;
+    if (e[0] == '0') return 0;
+    if (e[0] == 'a') return 2;
+    return 1;
+  }();
+  if (VBYTES == 32 && nvec > 0 && (bulk_mode == 2 || (bulk_mode == 1 && ent.bulk_default))) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_status(e, "tf_elementwise: device");
+    const unsigned bit = 1u << (dev & 31);
+    if (!(ent.bulk_attr_set.load(std::memory_order_acquire) & bit)) {
+      e = cudaFuncSetAttribute(ent.bulk_fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               ent.bulk_smem);
+      if (e != cudaSuccess) return cuda_status(e, "tf_elementwise: smem attribute");
+      ent.bulk_attr_set.fetch_or(bit, std::memory_order_acq_rel);
+    }
+    static const int breps = [] {
+      const char* r = getenv("TF_EW_BULK_REPS");
+      const int v = r ? atoi(r) : 0;
+      return (v >= 1 && v <= 256) ? v : 0;
+    }();
+    const int64_t ntile = (nvec + 255) / 256;
+    // keep at least ~4 CTAs per SM worth of chunks on small planes
+    int reps = breps ? breps : ent.bulk_reps;
+    while (reps > 1 && ntile / reps < 4LL * sm_count()) reps >>= 1;
+    int64_t blocks = (ntile + reps - 1) / reps;
+    const int64_t scal = head + (n - head - nvec * E);  // scalar head + tail elements
+    if (blocks < 1) blocks = 1;
+    if (blocks > 0x7fffffffLL) return fail(TF_EINVAL, "tf_elementwise: plane too long");
+    (void)scal;
+    Planes<double> p{};
+    for (int k = 0; k < ent.nin; k++) p.in[k] = static_cast<const double*>(in[k]);
+    p.out[0] = static_cast<double*>(out[0]);
+    p.out[1] = static_cast<double*>(out[1]);
+    void* args[] = {&p, &n, &head, &nvec, &reps};
+    e = launch_pdl(ent.bulk_fn, dim3((unsigned)blocks), dim3(256), args, ent.bulk_smem, stream);
+    return cuda_status(e, "tf_elementwise: launch");
   }
 
   int mbs = ent.max_blocks_per_sm.load(std::memory_order_relaxed);

@@ -94,26 +94,30 @@ __global__ void __launch_bounds__(256, TF_IL_MIN_BLOCKS) ew_il_kernel(ILArgs<T> 
       const int64_t j = base + u * 256;
       if (j >= nvec) continue;
       VP o;
+      T v[E][NIN];
 #pragma unroll
       for (int e = 0; e < E; e++) {
-        T v[NIN];
         if constexpr (XP) {
-          v[0] = xp[u].v[2 * e];
-          v[1] = xp[u].v[2 * e + 1];
+          v[e][0] = xp[u].v[2 * e];
+          v[e][1] = xp[u].v[2 * e + 1];
         } else {
-          v[0] = xs[u].v[e];
+          v[e][0] = xs[u].v[e];
         }
         if constexpr (AR == 22) {
-          v[2] = yp[u].v[2 * e];
-          v[3] = yp[u].v[2 * e + 1];
+          v[e][2] = yp[u].v[2 * e];
+          v[e][3] = yp[u].v[2 * e + 1];
         } else if constexpr (AR == 21) {
-          v[2] = ys[u].v[e];
+          v[e][2] = ys[u].v[e];
         } else if constexpr (AR == 11) {
-          v[1] = ys[u].v[e];
+          v[e][1] = ys[u].v[e];
         }
-        P<T> z = apply<T, OP>(v);
-        o.v[2 * e] = z.a;
-        o.v[2 * e + 1] = z.b;
+      }
+      P<T> z[E];
+      apply_lanes<T, OP, E>(v, z);
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        o.v[2 * e] = z[e].a;
+        o.v[2 * e + 1] = z[e].b;
       }
       st_stream(reinterpret_cast<VP*>(p.out) + j, o);
     }

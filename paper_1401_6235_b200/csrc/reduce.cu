@@ -56,36 +56,7 @@ __global__ void __launch_bounds__(RW) reduce_pair_kernel(const T* __restrict__ a
 // shared memory in exactly the canonical order (bank-conflict free: lane w reads
 // bytes [16w, 16w+16) of each 4 KB k-row).  NST stages in flight per CTA, two
 // CTAs per SM.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
+// (smem_u32 / mbar_* / bulk_g2s: common.cuh)
 
 template <int ROP>
 struct BulkGeo {
@@ -148,6 +119,7 @@ __global__ void __launch_bounds__(RW) reduce_bulk_kernel(const T* __restrict__ a
           else acc = fold<T, ROP>(acc, x, y);
         }
       }
+      fence_proxy_async_smem();  // generic reads before the async-proxy refill
       __syncthreads();  // every lane is done with this buffer
       if (w == 0 && j + G::NST < NSTAGES) issue(j + G::NST, buf);
     }

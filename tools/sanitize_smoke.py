@@ -61,6 +61,21 @@ for dt in (np.float64, np.float32):
     po = torch.empty_like(p)
     IL.vtadd2(p, p, po)
     F.vtaxpy(K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)), K.TwofoldArray(put(xs), put(xs)))
+# multi-tile elementwise launches (chunked CTAs; on the TMA-staged path several
+# shared-memory refills per CTA), misaligned head and a tail, every op
+for dt in (np.float64, np.float32):
+    n = (1 << 23) + 4099
+    for name in K.KERNELS:
+        spec = K.KERNELS[name]
+        nin = {"22": 4, "21": 3, "11": 2, "u2": 2, "u1": 1}[spec.arity]
+        ins = [rng.uniform(0.5, 2, n).astype(dt) for _ in range(nin)]
+        outs = [put(np.zeros(n, dt), 1) for _ in range(2)]
+        spec.loop(*[put(a, 1) for a in ins], *outs)
+        w = o.elementwise(name, *ins)
+        if not (np.array_equal(outs[0].cpu().numpy(), w[0]) and np.array_equal(outs[1].cpu().numpy(), w[1])):
+            bad += 1
+            print("mismatch (multi-tile)", name, dt, n)
+        del ins, outs, w
 # device batch (one launch, shared planes) and reduction pairs (one pass)
 for dt in (np.float64, np.float32):
     for n in (37, 4099, 3 * 65536 + 11):
