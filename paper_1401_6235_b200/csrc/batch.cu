@@ -20,6 +20,11 @@
 #include "common.cuh"
 #include "tf_math.cuh"
 
+// minimum resident CTAs requested for the batch kernel (A/B builds)
+#ifndef TF_BATCH_MINB
+#define TF_BATCH_MINB 1
+#endif
+
 namespace tf {
 
 constexpr int BMAX = 8;  // ops per launch
@@ -111,7 +116,7 @@ __device__ __forceinline__ void dispatch_elem(const BatchOp<T>& b, int64_t i) {
 // of the batch runs in order, so one plane's re-reads are a few hundred cycles
 // apart and hit L1.  Scalar head (common misalignment) and tail in the same launch.
 template <class T>
-__global__ void __launch_bounds__(256) batch_kernel(BatchArgs<T> a, int64_t n, int64_t head,
+__global__ void __launch_bounds__(256, TF_BATCH_MINB) batch_kernel(BatchArgs<T> a, int64_t n, int64_t head,
                                                     int64_t nvec, int reps) {
   constexpr int E = Vec32<T>::N;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -28,6 +28,14 @@
 #ifndef TF_SQRT_MINB
 #define TF_SQRT_MINB 1
 #endif
+// minimum resident CTAs requested for the other 32-byte-vector kernels (A/B builds)
+#ifndef TF_EW_MINB
+#define TF_EW_MINB 1
+#endif
+// minimum resident CTAs requested for the vtdiv2 vector kernel (A/B builds)
+#ifndef TF_DIV2_MINB
+#define TF_DIV2_MINB 1
+#endif
 // 32-byte vectors in flight per plane per thread for vtsqrt1: 1 (two IEEE square
 // roots and a division per element keep more elements in flight than registers
 // allow: U = 1 holds 56 registers, 4 CTAs per SM; U = 2 held 80-84, 3 CTAs, and
@@ -99,7 +107,9 @@ __device__ __forceinline__ void compute_store(const VecN<T, VB> (&r)[U][OpInfo<O
 }
 
 template <class T, int OP, int VB>
-__global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB : 1) ew_kernel(Planes<T> p, int64_t n, int64_t head,
+__global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB
+                                      : (OP == 3 && VB == 32) ? TF_DIV2_MINB
+                                      : VB == 32 ? TF_EW_MINB : 1) ew_kernel(Planes<T> p, int64_t n, int64_t head,
                                                  int64_t nvec, int reps) {
   constexpr int NIN = OpInfo<OP>::NIN;
   using V = VecN<T, VB>;
@@ -255,12 +265,14 @@ struct EwEntry {
   std::atomic<unsigned> bulk_attr_set;  // per-device bit: max dynamic smem raised
 };
 
-// Ops whose TMA-staged variant is the default (f64 ops with an IEEE division or
-// square root per element, A/B-measured on config-2 planes at 2^28:
-// profiles/r2_bulk_ab.txt).  TF_EW_BULK=0 / =all override it.
+// Ops whose TMA-staged variant is the default: none.  Measured against the
+// register path at 2^27/2^28 (profiles/r2_bulk_ab.txt): it wins only while the
+// SM clock sits at the power cap (vtsqrt1 +3.5% in a sustained loop) and loses
+// 0.5-5% at the bench's clocks, where the register path already keeps enough
+// bytes in flight.  TF_EW_BULK=all selects it for every op (A/B runs, tests).
 template <class T, int OP>
 constexpr bool bulk_default_op() {
-  return sizeof(T) == 8 && (OP == 3 || OP == 12);
+  return false;
 }
 
 template <class T, int OP, int VB>
