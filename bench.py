@@ -1659,7 +1659,8 @@ def _numba_reference_timing(wlname, inputs, ns, steps, warmup):
     del out1
     p = os.cpu_count() or 1
     ctx = mp.get_context("fork")
-    bar = ctx.Barrier(p + 1)
+    limit = 900.0  # a wedged or killed child must not hang the bench
+    bar = ctx.Barrier(p + 1, timeout=limit)
     q = ctx.Queue()
 
     def child(r):
@@ -1674,14 +1675,18 @@ def _numba_reference_timing(wlname, inputs, ns, steps, warmup):
         q.put(time.perf_counter() - t0)
         bar.wait()
 
-    procs = [ctx.Process(target=child, args=(r,)) for r in range(p)]
+    procs = [ctx.Process(target=child, args=(r,), daemon=True) for r in range(p)]
     for pr in procs:
         pr.start()
-    bar.wait()
-    bar.wait()
-    tp = max(q.get() for _ in procs)
-    for pr in procs:
-        pr.join()
+    try:
+        bar.wait()
+        bar.wait()
+        tp = max(q.get(timeout=limit) for _ in procs)
+    finally:
+        for pr in procs:
+            pr.join(timeout=5)
+            if pr.is_alive():
+                pr.terminate()
     nops = len(wl["names"])
     return {"value": nops * ns * steps / tp, "unit": "elem-ops/s", "cores": p,
             "sample": "%d elements per op x %d ops per step (%s), %d steps after %d warm-up, "

@@ -32,9 +32,12 @@
 #ifndef TF_EW_MINB
 #define TF_EW_MINB 1
 #endif
-// minimum resident CTAs requested for the vtdiv2 vector kernel (A/B builds)
+// minimum resident CTAs requested for the vtdiv2 vector kernel: 4 caps it at 64
+// registers (68 otherwise: 3 CTAs/SM) without spilling; +1.0% on config 2's vtdiv2
+// (6933 -> 7002 GB/s, profiles/r2s3_minb_ab.txt).  Capping every kernel at 64 lost
+// on vtdiv/vtsqrt (spills) and on the batch kernel.
 #ifndef TF_DIV2_MINB
-#define TF_DIV2_MINB 1
+#define TF_DIV2_MINB 4
 #endif
 // 32-byte vectors in flight per plane per thread for vtsqrt1: 1 (two IEEE square
 // roots and a division per element keep more elements in flight than registers
