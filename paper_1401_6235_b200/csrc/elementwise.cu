@@ -163,6 +163,70 @@ __global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB
   }
 }
 
+// The scalar head (common misalignment, < E elements) and tail (< E) as two
+// masked vectors, thread 0 the head and thread 1 the tail, through the vector
+// compute path (inactive lanes compute on 1.0 and are not stored).
+template <class T, int OP>
+__device__ __forceinline__ void head_tail(const Planes<T>& p, int64_t n, int64_t head,
+                                          int64_t nvec) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  using V = Vec32<T>;
+  constexpr int E = V::N;
+  if (threadIdx.x >= 2) return;
+  const int64_t s0 = threadIdx.x == 0 ? 0 : head + nvec * E;
+  const int64_t cnt = threadIdx.x == 0 ? head : n - s0;
+  if (cnt <= 0) return;
+  V r[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; k++)
+#pragma unroll
+    for (int e = 0; e < E; e++) r[k].v[e] = e < cnt ? p.in[k][s0 + e] : T(1);
+  V o0, o1;
+  apply_vec<T, OP, V, reg_fast_op<OP>()>(r, o0, o1);
+#pragma unroll
+  for (int e = 0; e < E; e++)
+    if (e < cnt) {
+      st_stream(p.out[0] + s0 + e, o0.v[e]);
+      st_stream(p.out[1] + s0 + e, o1.v[e]);
+    }
+}
+
+// ---- lean single-step kernel (the default for 32-byte vectors) ------------------
+// One CTA per 256*U vectors and nothing else: no chunk loop, no grid-stride
+// loops.  The scalar head (common misalignment, < E elements) and tail (< E)
+// ride in ONE extra CTA as two masked vectors — thread 0 the head, thread 1 the
+// tail — through the same per-lane compute, so the launch stays single.  Both
+// loops cost registers that the vector body pays for even when they never run:
+// vtsqrt1 holds 46 here against 56 in ew_kernel (5 resident CTAs per SM instead of
+// 4); ew_kernel stays for TF_EW_SCHED=persistent, TF_EW_REPS, 16-byte vectors and
+// mixed misalignment (profiles/r2s3_lean_ab.txt).
+template <class T, int OP>
+__global__ void __launch_bounds__(256, OP == 3 ? TF_DIV2_MINB : TF_EW_MINB)
+    ew_step_kernel(Planes<T> p, int64_t n, int64_t head, int64_t nvec, int64_t nblk) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  using V = Vec32<T>;
+  constexpr int U = (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : 2));
+  pdl_wait();
+  pdl_trigger();
+  if ((int64_t)blockIdx.x < nblk) {
+    const int64_t base = (int64_t)blockIdx.x * (256 * U) + threadIdx.x;
+    V r[U][NIN];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * 256;
+      if (j < nvec) {
+#pragma unroll
+        for (int k = 0; k < NIN; k++)
+          r[u][k] = ld_stream(reinterpret_cast<const V*>(p.in[k] + head) + j);
+      }
+    }
+    compute_store<T, OP, 32, U>(r, base, nvec, reinterpret_cast<V*>(p.out[0] + head),
+                                reinterpret_cast<V*>(p.out[1] + head));
+  } else {
+    head_tail<T, OP>(p, n, head, nvec);
+  }
+}
+
 // ---- TMA-staged variant: bulk async copies into a shared-memory ring ------------
 // Inputs arrive through cp.async.bulk (the TMA engine's UBLKCP) into NST stages of
 // one 256-vector tile (8 KB) per input plane.  Each thread reads its 32-byte
@@ -173,8 +237,9 @@ __global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB
 // path: two IEEE square roots and a division per element (~41 FP64 instructions)
 // leave warps computing, not loading, for most of their time.  Outputs leave as
 // 256-bit streaming stores straight from registers.  One CTA per chunk of `reps`
-// tiles (the hardware block scheduler balances the SMs); scalar head and tail as
-// in ew_kernel.  Same per-element core, so outputs are bit-identical to it.
+// tiles (the hardware block scheduler balances the SMs); the scalar head and tail
+// in one extra CTA (head_tail).  Same per-element core, so outputs are
+// bit-identical to ew_kernel.
 template <class T, int OP>
 struct BulkEw {
   static constexpr int NIN = OpInfo<OP>::NIN;
@@ -192,17 +257,14 @@ __global__ void __launch_bounds__(256) ew_bulk_kernel(Planes<T> p, int64_t n, in
   constexpr int E = V::N;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t bar[B::NST];
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   pdl_wait();
   pdl_trigger();
-  for (int64_t i = gtid; i < head; i += gstride) scalar_elem<T, OP>(p, i);
-  const int64_t tail0 = head + nvec * E;
-  for (int64_t i = tail0 + gtid; i < n; i += gstride) scalar_elem<T, OP>(p, i);
-
   const int64_t ntile = (nvec + 255) / 256;
   const int64_t t0 = (int64_t)blockIdx.x * reps;
-  if (t0 >= ntile) return;
+  if (t0 >= ntile) {  // the one extra CTA: scalar head and tail
+    head_tail<T, OP>(p, n, head, nvec);
+    return;
+  }
   const int cnt = (int)(ntile - t0 < reps ? ntile - t0 : reps);
   const T* src[NIN];
 #pragma unroll
@@ -239,7 +301,7 @@ __global__ void __launch_bounds__(256) ew_bulk_kernel(Planes<T> p, int64_t n, in
       for (int k = 0; k < NIN; k++)
         r[k] = *reinterpret_cast<const V*>(smem + (buf * NIN + k) * B::TILE + threadIdx.x * 32);
       V o0, o1;
-      apply_vec<T, OP>(r, o0, o1);
+      apply_vec<T, OP, V, reg_fast_op<OP>()>(r, o0, o1);
       st_stream(vo0 + jv, o0);
       st_stream(vo1 + jv, o1);
     }
@@ -261,6 +323,7 @@ struct EwEntry {
   int unroll;
   int reps;  // default chunk length in 256*unroll-vector steps (hbm sweep, profiles)
   std::atomic<int> max_blocks_per_sm;  // occupancy, filled lazily (idempotent)
+  const void* step_fn;  // lean single-step kernel (ew_step_kernel), 32-byte vectors only
   const void* bulk_fn;  // TMA-staged variant (ew_bulk_kernel), 32-byte vectors only
   int bulk_smem;
   int bulk_default;  // the bulk variant is the default for this op
@@ -291,6 +354,7 @@ EwEntry make_entry() {
                  U,
                  REPS,
                  {0},
+                 reinterpret_cast<const void*>(&ew_step_kernel<T, OP>),
                  reinterpret_cast<const void*>(&ew_bulk_kernel<T, OP>),
                  BulkEw<T, OP>::SMEM,
                  bulk_default_op<T, OP>(),
@@ -391,11 +455,9 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     // keep at least ~4 CTAs per SM worth of chunks on small planes
     int reps = breps ? breps : ent.bulk_reps;
     while (reps > 1 && ntile / reps < 4LL * sm_count()) reps >>= 1;
-    int64_t blocks = (ntile + reps - 1) / reps;
-    const int64_t scal = head + (n - head - nvec * E);  // scalar head + tail elements
-    if (blocks < 1) blocks = 1;
+    int64_t blocks = (ntile + reps - 1) / reps;  // >= 1: nvec > 0 here
+    if (head > 0 || n - head - nvec * E > 0) blocks++;  // the head_tail CTA
     if (blocks > 0x7fffffffLL) return fail(TF_EINVAL, "tf_elementwise: plane too long");
-    (void)scal;
     Planes<double> p{};
     for (int k = 0; k < ent.nin; k++) p.in[k] = static_cast<const double*>(in[k]);
     p.out[0] = static_cast<double*>(out[0]);
@@ -403,6 +465,37 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     void* args[] = {&p, &n, &head, &nvec, &reps};
     e = launch_pdl(ent.bulk_fn, dim3((unsigned)blocks), dim3(256), args, ent.bulk_smem, stream);
     return cuda_status(e, "tf_elementwise: launch");
+  }
+
+  // lean single-step kernel: the default for 32-byte vectors (TF_EW_LEAN=0, a
+  // TF_EW_REPS override or TF_EW_SCHED=persistent select ew_kernel)
+  static const bool lean = [] {
+    const char* e = getenv("TF_EW_LEAN");
+    return !(e && e[0] == '0');
+  }();
+  static const bool reps_override = [] {
+    const char* e = getenv("TF_EW_REPS");
+    return e && atoi(e) >= 1;
+  }();
+  static const bool persistent_env = [] {
+    const char* e = getenv("TF_EW_SCHED");
+    return e && e[0] == 'p';
+  }();
+  if (VBYTES == 32 && nvec > 0 && lean && !reps_override && !persistent_env) {
+    const int64_t per = 256LL * ent.unroll;
+    const int64_t nblk = (nvec + per - 1) / per;
+    const int64_t extra = (head > 0 || n - head - nvec * E > 0) ? 1 : 0;
+    if (nblk + extra <= 0x7fffffffLL) {
+      Planes<double> p{};
+      for (int k = 0; k < ent.nin; k++) p.in[k] = static_cast<const double*>(in[k]);
+      p.out[0] = static_cast<double*>(out[0]);
+      p.out[1] = static_cast<double*>(out[1]);
+      int64_t nb = nblk;
+      void* args[] = {&p, &n, &head, &nvec, &nb};
+      cudaError_t e = launch_pdl(ent.step_fn, dim3((unsigned)(nblk + extra)), dim3(256), args, 0,
+                                 stream);
+      return cuda_status(e, "tf_elementwise: launch");
+    }
   }
 
   int mbs = ent.max_blocks_per_sm.load(std::memory_order_relaxed);
