@@ -20,9 +20,12 @@
 #include "common.cuh"
 #include "tf_math.cuh"
 
-// minimum resident CTAs requested for the batch kernel (A/B builds)
+// minimum resident CTAs requested for the batch kernels (A/B builds)
 #ifndef TF_BATCH_MINB
 #define TF_BATCH_MINB 1
+#endif
+#ifndef TF_BATCH_STEP_MINB
+#define TF_BATCH_STEP_MINB 4
 #endif
 
 namespace tf {
@@ -73,6 +76,28 @@ __device__ __forceinline__ void batch_vec(const BatchOp<T>& b, int64_t head, int
   st_stream(reinterpret_cast<V*>(b.out[1] + head) + j, o1);
 }
 
+// cnt (< E) elements from s0 as one masked vector (inactive lanes compute on 1.0
+// and are not stored): the lean kernel's scalar head and tail
+template <class T, int OP>
+__device__ __forceinline__ void batch_masked(const BatchOp<T>& b, int64_t s0, int cnt) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  using V = Vec32<T>;
+  constexpr int E = V::N;
+  V r[NIN];
+#pragma unroll
+  for (int k = 0; k < NIN; k++)
+#pragma unroll
+    for (int e = 0; e < E; e++) r[k].v[e] = e < cnt ? b.in[k][s0 + e] : T(1);
+  V o0, o1;
+  apply_vec<T, OP, V, false>(r, o0, o1);
+#pragma unroll
+  for (int e = 0; e < E; e++)
+    if (e < cnt) {
+      st_stream(b.out[0] + s0 + e, o0.v[e]);
+      st_stream(b.out[1] + s0 + e, o1.v[e]);
+    }
+}
+
 template <class T, int OP>
 __device__ __forceinline__ void batch_elem(const BatchOp<T>& b, int64_t i) {
   constexpr int NIN = OpInfo<OP>::NIN;
@@ -94,6 +119,18 @@ __device__ __forceinline__ void dispatch_vec(const BatchOp<T>& b, int64_t head, 
 #define TF_CASE(ID) \
   case ID:          \
     batch_vec<T, ID>(b, head, j); \
+    break;
+    TF_BATCH_CASES(TF_CASE)
+#undef TF_CASE
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void dispatch_masked(const BatchOp<T>& b, int64_t s0, int cnt) {
+  switch (b.op) {
+#define TF_CASE(ID) \
+  case ID:          \
+    batch_masked<T, ID>(b, s0, cnt); \
     break;
     TF_BATCH_CASES(TF_CASE)
 #undef TF_CASE
@@ -138,6 +175,30 @@ __global__ void __launch_bounds__(256, TF_BATCH_MINB) batch_kernel(BatchArgs<T> 
   }
 }
 
+// Lean variant (the f64 default when every plane shares the 32-byte alignment): one
+// CTA per 256 vectors and no loops but the ops, the scalar head and tail as masked
+// vectors in one extra CTA (thread 0 head, thread 1 tail) — the loops of
+// batch_kernel cost registers the vector body pays for (as ew_step_kernel).
+template <class T>
+__global__ void __launch_bounds__(256, TF_BATCH_STEP_MINB) batch_step_kernel(BatchArgs<T> a, int64_t n,
+                                                                        int64_t head, int64_t nvec,
+                                                                        int64_t nblk) {
+  constexpr int E = Vec32<T>::N;
+  const int nops = a.nops;
+  if ((int64_t)blockIdx.x < nblk) {
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (j < nvec)
+#pragma unroll 1
+      for (int o = 0; o < nops; o++) dispatch_vec<T>(a.o[o], head, j);
+  } else if (threadIdx.x < 2) {
+    const int64_t s0 = threadIdx.x == 0 ? 0 : head + nvec * E;
+    const int cnt = (int)(threadIdx.x == 0 ? head : n - s0);
+    if (cnt > 0)
+#pragma unroll 1
+      for (int o = 0; o < nops; o++) dispatch_masked<T>(a.o[o], s0, cnt);
+  }
+}
+
 int ew_num_inputs(int op);
 
 template <class T>
@@ -168,6 +229,21 @@ static int launch_batch(int nops, const int* ops, int64_t n, const void* const* 
     head = mis ? (int64_t)((32 - mis) / tsz) : 0;
     if (head > n) head = n;
     nvec = (n - head) / E;
+  }
+  static const bool lean = [] {  // TF_BATCH_LEAN=0 / TF_BATCH_REPS select batch_kernel (A/B)
+    const char* e = getenv("TF_BATCH_LEAN");
+    const char* r = getenv("TF_BATCH_REPS");
+    return !(e && e[0] == '0') && !(r && atoi(r) >= 1);
+  }();
+  // f64 only: +1.8% on config 2's five-op batch, while f32 measured 2% slower than
+  // batch_kernel on config 3 (profiles/r2s3_batch_ab.txt)
+  if (lean && nvec > 0 && sizeof(T) == 8) {
+    const int64_t nblk = (nvec + 255) / 256;
+    const int64_t extra = (head > 0 || n - head - nvec * E > 0) ? 1 : 0;
+    if (nblk + extra <= 0x7fffffffLL) {
+      batch_step_kernel<T><<<(unsigned)(nblk + extra), 256, 0, s>>>(a, n, head, nvec, nblk);
+      return launch_status("tf_elementwise_batch: launch");
+    }
   }
   int mbs = mbs_cache.load(std::memory_order_relaxed);
   if (mbs == 0) {

@@ -14,6 +14,8 @@
 // (same launch).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tf_math.cuh"
 
@@ -132,6 +134,105 @@ __global__ void __launch_bounds__(256, TF_IL_MIN_BLOCKS) ew_il_kernel(ILArgs<T> 
   }
 }
 
+// Lean variant (the default when the arrays are aligned): one CTA per 256*U
+// steps, no chunk or grid-stride loops; the n % E remainder rides in one extra CTA
+// as a masked step through the same per-lane compute (as ew_step_kernel).
+#ifndef TF_IL_STEP_MIN_BLOCKS
+#define TF_IL_STEP_MIN_BLOCKS 4
+#endif
+template <class T, int OP>
+__global__ void __launch_bounds__(256, TF_IL_STEP_MIN_BLOCKS) ew_il_step_kernel(ILArgs<T> p, int64_t n, int64_t nblk) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  constexpr int AR = OpInfo<OP>::ARITY;
+  constexpr int E = Vec16<T>::N;
+  const int64_t nvec = n / E;
+
+  // one step = E elements: a pair operand is one 32-byte vector (E pairs,
+  // sm_100 256-bit LDG), a plain plane one 16-byte vector; the result one
+  // 32-byte store.
+  using VP = Vec32<T>;   // E pairs
+  using VS = Vec16A<T>;  // E scalars
+  constexpr bool XP = (AR == 22 || AR == 21 || AR == 2);
+  // steps in flight per thread (all loads issue before any math); the one-plane
+  // op (vtsqrt: 16 bytes in per step) carries 4 to keep enough bytes in flight
+  constexpr int U = AR == 1 ? 4 : 2;
+  // CTA-chunked, as the split kernels: chunk = 256*U consecutive steps per CTA,
+  // thread t takes steps t and t+256 (coalesced, contiguous per CTA)
+  const int64_t CH = 256LL * U;
+  if ((int64_t)blockIdx.x < nblk) {
+    const int64_t cb = (int64_t)blockIdx.x * CH;
+    const int64_t base = cb + threadIdx.x;
+    VP xp[U], yp[U];
+    VS xs[U], ys[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * 256;
+      if (j < nvec) {
+        if constexpr (XP) xp[u] = ld_stream(reinterpret_cast<const VP*>(p.a) + j);
+        else xs[u] = ld_stream(reinterpret_cast<const VS*>(p.a) + j);
+        if constexpr (AR == 22) yp[u] = ld_stream(reinterpret_cast<const VP*>(p.b) + j);
+        else if constexpr (AR == 21 || AR == 11) ys[u] = ld_stream(reinterpret_cast<const VS*>(p.b) + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * 256;
+      if (j >= nvec) continue;
+      VP o;
+      T v[E][NIN];
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        if constexpr (XP) {
+          v[e][0] = xp[u].v[2 * e];
+          v[e][1] = xp[u].v[2 * e + 1];
+        } else {
+          v[e][0] = xs[u].v[e];
+        }
+        if constexpr (AR == 22) {
+          v[e][2] = yp[u].v[2 * e];
+          v[e][3] = yp[u].v[2 * e + 1];
+        } else if constexpr (AR == 21) {
+          v[e][2] = ys[u].v[e];
+        } else if constexpr (AR == 11) {
+          v[e][1] = ys[u].v[e];
+        }
+      }
+      P<T> z[E];
+      apply_lanes<T, OP, E>(v, z);
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        o.v[2 * e] = z[e].a;
+        o.v[2 * e + 1] = z[e].b;
+      }
+      st_stream(reinterpret_cast<VP*>(p.out) + j, o);
+    }
+  } else if (threadIdx.x == 0) {
+    // the n % E remainder as one masked step (inactive lanes compute on 1.0)
+    const int64_t i0 = nvec * E;
+    const int cnt = (int)(n - i0);
+    if (cnt > 0) {
+      T v[E][NIN];
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        if (e < cnt) {
+          il_gather<T, OP>(p, i0 + e, v[e]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < NIN; k++) v[e][k] = T(1);
+        }
+      }
+      P<T> z[E];
+      apply_lanes<T, OP, E>(v, z);
+#pragma unroll
+      for (int e = 0; e < E; e++)
+        if (e < cnt) {
+          st_stream(p.out + 2 * (i0 + e), z[e].a);
+          st_stream(p.out + 2 * (i0 + e) + 1, z[e].b);
+        }
+    }
+  }
+}
+
 template <class T>
 __global__ void __launch_bounds__(256) interleave_kernel(const T* __restrict__ v,
                                                          const T* __restrict__ e,
@@ -194,11 +295,13 @@ __global__ void __launch_bounds__(256) deinterleave_kernel(const T* __restrict__
 
 struct IlEntry {
   const void* fn;
+  const void* step_fn;  // lean variant (aligned arrays)
 };
 
 template <class T, int OP>
 IlEntry make_il() {
-  return IlEntry{reinterpret_cast<const void*>(&ew_il_kernel<T, OP>)};
+  return IlEntry{reinterpret_cast<const void*>(&ew_il_kernel<T, OP>),
+                 reinterpret_cast<const void*>(&ew_il_step_kernel<T, OP>)};
 }
 template <class T, int... OPS>
 struct IlTable {
@@ -244,6 +347,21 @@ int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* 
   ILArgs<double> p{static_cast<const double*>(a), static_cast<const double*>(b ? b : a),
                    static_cast<double*>(out)};
   const int U = ar == 1 ? 4 : 2;  // steps per thread, as in ew_il_kernel
+  static const bool lean = [] {  // TF_IL_LEAN=0 selects ew_il_kernel (A/B)
+    const char* e = getenv("TF_IL_LEAN");
+    return !(e && e[0] == '0');
+  }();
+  if (vec && lean && n >= E) {
+    const int64_t nblk = (n / E + 256LL * U - 1) / (256LL * U);
+    const int64_t extra = n % E ? 1 : 0;
+    if (nblk + extra <= 0x7fffffffLL) {
+      int64_t nb = nblk;
+      void* args[] = {&p, &n, &nb};
+      return cuda_status(
+          cudaLaunchKernel(ent.step_fn, dim3((unsigned)(nblk + extra)), dim3(256), args, 0, s),
+          "tf_elementwise_il: launch");
+    }
+  }
   const int64_t blocks = grid_for(vec ? (n / E + U - 1) / U : n);
   void* args[] = {&p, &n, &vec};
   return cuda_status(cudaLaunchKernel(ent.fn, dim3((unsigned)blocks), dim3(256), args, 0, s),

@@ -115,17 +115,19 @@ def test_interleaved_large_matches_split():
     from paper_1401_6235_b200 import kernels as K
     from paper_1401_6235_b200 import workloads as W
 
-    n = (1 << 22) + 1
-    ps = W.PlaneSet("config2", n, torch.float64, 0)
-    for name in ("vtadd2", "vtdiv2", "vtsqrt1"):
-        planes = ps.planes(name)
-        out = K.empty_twofold(n, torch.float64)
-        K.KERNELS[name].loop(*planes, *out)
-        x = IL.from_split(K.TwofoldArray(planes[0], planes[1]))
-        args = (x,) if name == "vtsqrt1" else (x, IL.from_split(K.TwofoldArray(planes[2], planes[3])))
-        po = IL.empty_pairs(n)
-        IL.KERNELS[name](*args, po)
-        assert torch.equal(po[:, 0], out.value) and torch.equal(po[:, 1], out.error)
+    # odd lengths: the n % E remainder takes the lean kernel's masked step
+    for cfg, n, dt, names in (("config2", (1 << 22) + 1, torch.float64, ("vtadd2", "vtdiv2", "vtsqrt1")),
+                              ("config3", (1 << 22) + 3, torch.float32, ("vtadd2", "vtmul2", "vtdiv2"))):
+        ps = W.PlaneSet(cfg, n, dt, 0)
+        for name in names:
+            planes = ps.planes(name)
+            out = K.empty_twofold(n, dt)
+            K.KERNELS[name].loop(*planes, *out)
+            x = IL.from_split(K.TwofoldArray(planes[0], planes[1]))
+            args = (x,) if name == "vtsqrt1" else (x, IL.from_split(K.TwofoldArray(planes[2], planes[3])))
+            po = IL.empty_pairs(n, dt)
+            IL.KERNELS[name](*args, po)
+            assert torch.equal(po[:, 0], out.value) and torch.equal(po[:, 1], out.error), (name, dt)
 
 
 def test_interleaved_validation_without_gpu():
