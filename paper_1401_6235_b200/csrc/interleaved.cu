@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(256, TF_IL_MIN_BLOCKS) ew_il_kernel(ILArgs<T> 
   }
 }
 
-// Lean variant (the default when the arrays are aligned): one CTA per 256*U
+// Lean variant (aligned arrays; the default only where it measured faster, see
+// il_lean_default): one CTA per 256*U
 // steps, no chunk or grid-stride loops; the n % E remainder rides in one extra CTA
 // as a masked step through the same per-lane compute (as ew_step_kernel).
 #ifndef TF_IL_STEP_MIN_BLOCKS
@@ -296,12 +297,22 @@ __global__ void __launch_bounds__(256) deinterleave_kernel(const T* __restrict__
 struct IlEntry {
   const void* fn;
   const void* step_fn;  // lean variant (aligned arrays)
+  bool lean_default;    // the lean variant measured faster for this op
 };
+
+// Ops whose lean interleaved kernel is the default: f32 vtsqrt1 and vtdiv (+4.6%,
+// +2.1% at 2^27); for the rest ew_il_kernel was 0.3-1.5% faster
+// (profiles/r2s3_il_lean_ab.txt).  TF_IL_LEAN=1 / =0 force either for every op.
+template <class T, int OP>
+constexpr bool il_lean_default() {
+  return sizeof(T) == 4 && (OP == 11 || OP == 12);
+}
 
 template <class T, int OP>
 IlEntry make_il() {
   return IlEntry{reinterpret_cast<const void*>(&ew_il_kernel<T, OP>),
-                 reinterpret_cast<const void*>(&ew_il_step_kernel<T, OP>)};
+                 reinterpret_cast<const void*>(&ew_il_step_kernel<T, OP>),
+                 il_lean_default<T, OP>()};
 }
 template <class T, int... OPS>
 struct IlTable {
@@ -347,10 +358,11 @@ int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* 
   ILArgs<double> p{static_cast<const double*>(a), static_cast<const double*>(b ? b : a),
                    static_cast<double*>(out)};
   const int U = ar == 1 ? 4 : 2;  // steps per thread, as in ew_il_kernel
-  static const bool lean = [] {  // TF_IL_LEAN=0 selects ew_il_kernel (A/B)
+  static const int lean_env = [] {  // -1 per-op default, 0 never, 1 always
     const char* e = getenv("TF_IL_LEAN");
-    return !(e && e[0] == '0');
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
   }();
+  const bool lean = lean_env < 0 ? ent.lean_default : lean_env == 1;
   if (vec && lean && n >= E) {
     const int64_t nblk = (n / E + 256LL * U - 1) / (256LL * U);
     const int64_t extra = n % E ? 1 : 0;

@@ -17,7 +17,7 @@ ROOT = Path(__file__).resolve().parents[1]
 
 VARIANTS = [{}, {"TF_VEC_BYTES": "16"}, {"TF_EW_SCHED": "persistent"},
             {"TF_EW_BULK": "0"}, {"TF_EW_BULK": "all"}, {"TF_EW_BULK": "all", "TF_EW_BULK_REPS": "3"},
-            {"TF_EW_LEAN": "0"}, {"TF_EW_REPS": "2"}, {"TF_BATCH_LEAN": "0"}, {"TF_IL_LEAN": "0"},
+            {"TF_EW_LEAN": "0"}, {"TF_EW_REPS": "2"}, {"TF_BATCH_LEAN": "0"}, {"TF_IL_LEAN": "1"},
             {"TF_REDUCE_PATH": "bulk"}, {"TF_HOST_SLOTS": "2", "TF_HOST_CHUNK_MB": "1"},
             {"TF_HOST_ZEROCOPY_MB": "0"}, {"TF_HOST_ZEROCOPY_MB": "4096"}]
 
