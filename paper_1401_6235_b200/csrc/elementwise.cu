@@ -87,7 +87,7 @@ __device__ __forceinline__ void scalar_elem(const Planes<T>& p, int64_t i) {
 // intrinsics at the hbm size (profiles/r2_fastpath_ab.txt): vtdiv and vtsqrt,
 // +12% and +6%.  For vtdiv2 and vtsqrt1 the interleaved lanes raise registers
 // past four resident CTAs per SM and cost more bytes in flight than the ILP
-// gains; those run on the TMA-staged path (ew_bulk_kernel) instead.
+// gains; those keep the intrinsics.
 template <int OP>
 __host__ __device__ constexpr bool reg_fast_op() {
   return OP == 11 || OP == 13;
