@@ -988,6 +988,7 @@ def run_elementwise(args, rank, world, local, wlname):
     if rank != 0:
         return None
     d = per_op[dom]
+    step_gbs = world * bytes_per_step * K / (tm["elapsed_ms"] * 1e-3) / 1e9
     return {
         "metric": METRIC if wlname == "config2" else METRIC + " [%s]" % wlname,
         "value": value, "unit": "elem-ops/s", "n_gpus": world,
@@ -1007,11 +1008,18 @@ def run_elementwise(args, rank, world, local, wlname):
             "l2": ("working set %d MiB < L2 x3: flushed" if tm["flush"] else
                    "working set %d MiB >> 126 MB L2; no flush") % (ws_bytes >> 20),
             "n_this_rank": n},
-        "hbm_gbs": world * bytes_per_step * K / (tm["elapsed_ms"] * 1e-3) / 1e9,
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak,
-                     "unit": "GB/s", "frac": d["gbs"] / peak,
-                     "traffic": ncu_traffic(dom, dts, n),
-                     "algorithmic_bytes": d["bytes"], "peak_source": peak_src},
+        "hbm_gbs": step_gbs,
+        "roofline": dict(
+            {"bound": "hbm", "kernel": dom, "achieved": d["gbs"], "peak": peak,
+             "unit": "GB/s", "frac": d["gbs"] / peak,
+             "traffic": ncu_traffic(dom, dts, n),
+             "algorithmic_bytes": d["bytes"], "peak_source": peak_src},
+            # launch-bound steps: `achieved` is one launch alone (events around an eager
+            # launch, their latency included); the whole step's bytes over the step's
+            # time — the concurrent graph branches together — is the rate HBM saw
+            **({"step": {"achieved": step_gbs / world, "frac": step_gbs / world / peak,
+                         "what": "all launches of one graph replay, bytes / step time"}}
+               if tm["use_graph"] else {})),
         "per_op": per_op,
         "cpu_baseline": cpu,
         "e2e": e2e,

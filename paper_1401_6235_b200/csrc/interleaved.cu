@@ -292,6 +292,106 @@ __global__ void __launch_bounds__(256) deinterleave_kernel(const T* __restrict__
   }
 }
 
+// ---- lean conversions (the default for 32-byte-aligned arrays) ---------------------
+// One CTA per 256*2 vector steps and no loops: a step moves E = 32/sizeof(T)
+// elements — two 32-byte loads (one per plane, or two adjacent pair vectors) and two
+// 32-byte stores, both steps' loads issued before any store.  The n % E tail rides in
+// one extra CTA, one element per thread.  Pure data movement at the vmem copy's 1:1
+// read/write mix (16 B in, 16 B out per f64 element).  Measured at 2^27/2^28
+// (tools/convert_bench.py, profiles/r2s5_convert_ab.txt): f64 interleave 6.54 ->
+// 6.92 TB/s (+6%); the other three conversions ran 1.4-2.3% faster on the 16-byte
+// grid-stride kernels above (6.87-7.07 TB/s), so those keep them.  TF_CONV_LEAN=1 /
+// =0 force either variant for every conversion (A/B, tests).
+template <class T>
+__global__ void __launch_bounds__(256) interleave_step_kernel(const T* __restrict__ v,
+                                                              const T* __restrict__ e,
+                                                              T* __restrict__ out, int64_t n,
+                                                              int64_t nvec, int64_t nblk) {
+  using V = Vec32<T>;
+  constexpr int E = V::N;
+  constexpr int U = 2;
+  if ((int64_t)blockIdx.x < nblk) {
+    const int64_t base = (int64_t)blockIdx.x * (256 * U) + threadIdx.x;
+    V a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * 256;
+      if (j < nvec) {
+        a[u] = ld_stream(reinterpret_cast<const V*>(v) + j);
+        b[u] = ld_stream(reinterpret_cast<const V*>(e) + j);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * 256;
+      if (j < nvec) {
+        V o0, o1;
+#pragma unroll
+        for (int k = 0; k < E / 2; k++) {
+          o0.v[2 * k] = a[u].v[k];
+          o0.v[2 * k + 1] = b[u].v[k];
+          o1.v[2 * k] = a[u].v[E / 2 + k];
+          o1.v[2 * k + 1] = b[u].v[E / 2 + k];
+        }
+        V* po = reinterpret_cast<V*>(out) + 2 * j;
+        st_stream(po, o0);
+        st_stream(po + 1, o1);
+      }
+    }
+  } else {
+    const int64_t i = nvec * E + threadIdx.x;
+    if (i < n) {
+      st_stream(out + 2 * i, ld_stream(v + i));
+      st_stream(out + 2 * i + 1, ld_stream(e + i));
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) deinterleave_step_kernel(const T* __restrict__ in,
+                                                                T* __restrict__ v,
+                                                                T* __restrict__ e, int64_t n,
+                                                                int64_t nvec, int64_t nblk) {
+  using V = Vec32<T>;
+  constexpr int E = V::N;
+  constexpr int U = 2;
+  if ((int64_t)blockIdx.x < nblk) {
+    const int64_t base = (int64_t)blockIdx.x * (256 * U) + threadIdx.x;
+    V r0[U], r1[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * 256;
+      if (j < nvec) {
+        const V* pi = reinterpret_cast<const V*>(in) + 2 * j;
+        r0[u] = ld_stream(pi);
+        r1[u] = ld_stream(pi + 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t j = base + u * 256;
+      if (j < nvec) {
+        V a, b;
+#pragma unroll
+        for (int k = 0; k < E / 2; k++) {
+          a.v[k] = r0[u].v[2 * k];
+          b.v[k] = r0[u].v[2 * k + 1];
+          a.v[E / 2 + k] = r1[u].v[2 * k];
+          b.v[E / 2 + k] = r1[u].v[2 * k + 1];
+        }
+        st_stream(reinterpret_cast<V*>(v) + j, a);
+        st_stream(reinterpret_cast<V*>(e) + j, b);
+      }
+    }
+  } else {
+    const int64_t i = nvec * E + threadIdx.x;
+    if (i < n) {
+      st_stream(v + i, ld_stream(in + 2 * i));
+      st_stream(e + i, ld_stream(in + 2 * i + 1));
+    }
+  }
+}
+
 // ---- dispatch ------------------------------------------------------------------
 
 struct IlEntry {
@@ -386,6 +486,39 @@ int convert_launch(int to_interleaved, int dtype, int64_t n, const void* a, cons
     return fail(TF_EINVAL, "tf_interleave: bad arguments");
   if (n == 0) return TF_OK;
   const int E = dtype == TF_F64 ? 2 : 4;
+  if (!a || !b || !c)
+    return fail(TF_EINVAL, to_interleaved ? "tf_interleave: null array"
+                                          : "tf_deinterleave: null array");
+  static const int lean_env = [] {  // -1 per-conversion default, 0 never, 1 always
+    const char* e = getenv("TF_CONV_LEAN");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  const bool lean = lean_env < 0 ? (to_interleaved && dtype == TF_F64) : lean_env == 1;
+  const int64_t E32 = 2 * E;  // elements per 32-byte vector
+  if (lean && n >= E32 && aligned32(a) && aligned32(b) && aligned32(c)) {
+    const int64_t nvec = n / E32;
+    const int64_t nblk = (nvec + 511) / 512;
+    const int64_t extra = n % E32 ? 1 : 0;
+    if (nblk + extra <= 0x7fffffffLL) {
+      const unsigned grid = (unsigned)(nblk + extra);
+      if (to_interleaved) {
+        if (dtype == TF_F64)
+          interleave_step_kernel<double><<<grid, 256, 0, s>>>((const double*)a, (const double*)b,
+                                                             (double*)c, n, nvec, nblk);
+        else
+          interleave_step_kernel<float><<<grid, 256, 0, s>>>((const float*)a, (const float*)b,
+                                                            (float*)c, n, nvec, nblk);
+      } else {
+        if (dtype == TF_F64)
+          deinterleave_step_kernel<double><<<grid, 256, 0, s>>>(
+              (const double*)a, (double*)const_cast<void*>(b), (double*)c, n, nvec, nblk);
+        else
+          deinterleave_step_kernel<float><<<grid, 256, 0, s>>>(
+              (const float*)a, (float*)const_cast<void*>(b), (float*)c, n, nvec, nblk);
+      }
+      return launch_status(to_interleaved ? "tf_interleave" : "tf_deinterleave");
+    }
+  }
   if (to_interleaved) {  // a = value, b = error, c = pairs
     if (!a || !b || !c) return fail(TF_EINVAL, "tf_interleave: null array");
     int vec = aligned16(a) && aligned16(b) && aligned16(c);

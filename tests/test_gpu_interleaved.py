@@ -109,6 +109,51 @@ def test_conversions_round_trip(dtype):
         assert torch.equal(back.value, v) and torch.equal(back.error, e)
 
 
+_CONV_SWEEP = r"""
+import torch
+from paper_1401_6235_b200 import interleaved as IL, kernels as K
+for dtype in (torch.float64, torch.float32):
+    E = 32 // torch.empty(0, dtype=dtype).element_size()
+    sizes = sorted({1, E - 1, E, E + 1, 2 * E + 1, 255 * E, 256 * E, 512 * E - 1, 512 * E,
+                    512 * E + 1, 1024 * E + E // 2, (1 << 21) + 5})
+    for n in sizes:
+        for off in (0, 1, 4):  # views off the 32-byte alignment take the 16-byte / scalar kernels
+            vb = torch.randn(n + off, dtype=dtype, device="cuda")
+            eb = torch.randn(n + off, dtype=dtype, device="cuda")
+            v, e = vb[off:], eb[off:]
+            G = E // 2  # guard rows: E/2 pairs = 32 bytes, so an aligned base stays aligned
+            guard = torch.full((n + 2 * G, 2), 7.0, dtype=dtype, device="cuda")
+            p = guard[G:n + G]
+            IL.from_split(K.TwofoldArray(v, e), p)
+            assert torch.equal(p[:, 0], v) and torch.equal(p[:, 1], e), (dtype, n, off)
+            assert (guard[:G] == 7).all() and (guard[n + G:] == 7).all(), (dtype, n, off)
+            ob = [torch.full((n + off + 2 * E,), 7.0, dtype=dtype, device="cuda") for _ in range(2)]
+            o = K.TwofoldArray(ob[0][off + E:off + E + n], ob[1][off + E:off + E + n])
+            IL.to_split(p, o)
+            assert torch.equal(o.value, v) and torch.equal(o.error, e), (dtype, n, off)
+            for b in ob:
+                assert (b[:off + E] == 7).all() and (b[off + E + n:] == 7).all(), (dtype, n, off)
+print("conv-ok")
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lean", ["1", "0", None])
+def test_conversions_sweep_both_variants(lean):
+    # lean 32-byte step kernels (default) and the 16-byte grid-stride kernels
+    # (TF_CONV_LEAN=0): sizes around the vector and CTA boundaries, aligned and
+    # misaligned views, guard elements either side of every destination
+    import os, subprocess, sys
+    env = dict(os.environ)
+    env.pop("TF_CONV_LEAN", None)
+    if lean is not None:
+        env["TF_CONV_LEAN"] = lean
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", _CONV_SWEEP], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "conv-ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
+
+
 @pytest.mark.gpu
 def test_interleaved_large_matches_split():
     from paper_1401_6235_b200 import interleaved as IL

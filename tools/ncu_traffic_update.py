@@ -3,6 +3,9 @@ into profiles/ncu_traffic.json, keyed "op|dtype|n" (bench.ncu_traffic), and a
 per-kernel summary next to it.
 
     python tools/ncu_traffic_update.py gpurun_out/ns_config2.ncu-rep ... --tag r2
+
+A `.summary.json` (tools/ncu_summary.py --json, written on the GPU box when the reports
+are too large to bring back) is accepted in place of a report.
 """
 import json
 import re
@@ -48,7 +51,8 @@ def main():
     summary = []
     for rep in args:
         cfg = re.search(r"(config\d)", rep).group(1)
-        for d in summarise(rep):
+        rows = json.loads(Path(rep).read_text()) if rep.endswith(".json") else summarise(rep)
+        for d in rows:
             op, dt = op_of(d["kernel"])
             if op is None:
                 continue
@@ -59,7 +63,7 @@ def main():
                    "warps_active_pct": d.get("warps_active_pct"),
                    "fp64_pipe_pct": d.get("fp64_pipe_pct"), "fp64_inst": d.get("fp64_inst"),
                    "source": "%s (%s, ncu --set full --clock-control none)"
-                             % (Path(rep).name, tag)}
+                             % (Path(rep).name.replace(".summary.json", ".ncu-rep"), tag)}
             table[key] = rec
             summary.append(dict(key=key, kernel=d["kernel"][:90], **rec))
     path.write_text(json.dumps(dict(sorted(table.items())), indent=1) + "\n")
