@@ -227,6 +227,46 @@ __global__ void __launch_bounds__(256, OP == 3 ? TF_DIV2_MINB : TF_EW_MINB)
   }
 }
 
+// ---- lean 16-byte variant (vtsqrt1's default) --------------------------------------
+// The same single-step structure with ONE 16-byte vector per plane per thread and a
+// 32-register cap (__launch_bounds__(256, 8): eight resident CTAs, 2048 threads per SM).
+// For vtsqrt1 — two IEEE square roots and a division per element, a 1:1 read/write mix
+// — more, lighter threads beat fewer, fatter ones: the latency of the dependent
+// sqrt/div chains is hidden by occupancy instead of by per-thread ILP
+// (tools/micro/mix11.cu: 7.01-7.03 TB/s against 6.74-6.83 for the 32-byte kernel;
+// profiles/r2s5_mix11.txt).  Alignment contract as ew_step_kernel (head to the 32-byte
+// boundary, nvec counts 32-byte vectors); the head and tail elements run scalar in one
+// extra CTA, one element per thread.  TF_EW_V16 selects the ops (A/B): unset = the
+// per-op default, 0 = none, all = every op.
+// (the three- and four-plane division ops spill at 32 registers: 40-48 for those)
+template <class T, int OP>
+__global__ void __launch_bounds__(256, OP == 3 ? 5 : (OP == 7 || OP == 17 || OP == 21) ? 6 : 8)
+    ew_step16_kernel(Planes<T> p, int64_t n, int64_t head, int64_t nvec16, int64_t nblk) {
+  constexpr int NIN = OpInfo<OP>::NIN;
+  using V = Vec16A<T>;
+  constexpr int E = V::N;
+  pdl_wait();
+  pdl_trigger();
+  if ((int64_t)blockIdx.x < nblk) {
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (j < nvec16) {
+      V r[NIN];
+#pragma unroll
+      for (int k = 0; k < NIN; k++) r[k] = ld_stream(reinterpret_cast<const V*>(p.in[k] + head) + j);
+      V o0, o1;
+      apply_vec<T, OP, V, false>(r, o0, o1);
+      st_stream(reinterpret_cast<V*>(p.out[0] + head) + j, o0);
+      st_stream(reinterpret_cast<V*>(p.out[1] + head) + j, o1);
+    }
+  } else {
+    // head: elements [0, head); tail: [head + nvec16*E, n) — fewer than 32/sizeof(T) each
+    const int64_t t0 = head + nvec16 * E;
+    const int64_t i = (int64_t)threadIdx.x < head ? (int64_t)threadIdx.x
+                                                  : t0 + ((int64_t)threadIdx.x - head);
+    if (i < head || (i >= t0 && i < n)) scalar_elem<T, OP>(p, i);
+  }
+}
+
 // ---- TMA-staged variant: bulk async copies into a shared-memory ring ------------
 // Inputs arrive through cp.async.bulk (the TMA engine's UBLKCP) into NST stages of
 // one 256-vector tile (8 KB) per input plane.  Each thread reads its 32-byte
@@ -329,7 +369,15 @@ struct EwEntry {
   int bulk_default;  // the bulk variant is the default for this op
   int bulk_reps;     // tiles per CTA
   std::atomic<unsigned> bulk_attr_set;  // per-device bit: max dynamic smem raised
+  const void* step16_fn;  // lean 16-byte variant
+  bool v16_default;       // ... is the default for this op
 };
+
+// Ops whose lean 16-byte kernel is the default (measured, profiles/r2s5_v16_ab.txt)
+template <class T, int OP>
+constexpr bool v16_default_op() {
+  return sizeof(T) == 8 && OP == 12;
+}
 
 // Ops whose TMA-staged variant is the default: none.  Measured against the
 // register path at 2^27/2^28 (profiles/r2_bulk_ab.txt): it wins only while the
@@ -359,7 +407,9 @@ EwEntry make_entry() {
                  BulkEw<T, OP>::SMEM,
                  bulk_default_op<T, OP>(),
                  NIN <= 2 ? 8 : 4,
-                 {0u}};
+                 {0u},
+                 reinterpret_cast<const void*>(&ew_step16_kernel<T, OP>),
+                 v16_default_op<T, OP>()};
 }
 
 template <class T, int VB, int... OPS>
@@ -481,6 +531,29 @@ int ew_launch(int op, int dtype, int64_t n, const void* const* in, void* const* 
     const char* e = getenv("TF_EW_SCHED");
     return e && e[0] == 'p';
   }();
+  static const int v16_mode = [] {  // 0 never, 1 per-op default, 2 every op
+    const char* e = getenv("TF_EW_V16");
+    if (!e) return 1;
+    if (e[0] == '0') return 0;
+    return e[0] == 'a' ? 2 : 1;
+  }();
+  if (VBYTES == 32 && nvec > 0 && lean && !reps_override && !persistent_env &&
+      (v16_mode == 2 || (v16_mode == 1 && ent.v16_default))) {
+    const int64_t nvec16 = nvec * 2;
+    const int64_t nblk = (nvec16 + 255) / 256;
+    const int64_t extra = (head > 0 || n - head - nvec * E > 0) ? 1 : 0;
+    if (nblk + extra <= 0x7fffffffLL) {
+      Planes<double> p{};
+      for (int k = 0; k < ent.nin; k++) p.in[k] = static_cast<const double*>(in[k]);
+      p.out[0] = static_cast<double*>(out[0]);
+      p.out[1] = static_cast<double*>(out[1]);
+      int64_t nb = nblk, nv = nvec16;
+      void* args[] = {&p, &n, &head, &nv, &nb};
+      cudaError_t e = launch_pdl(ent.step16_fn, dim3((unsigned)(nblk + extra)), dim3(256), args,
+                                 0, stream);
+      return cuda_status(e, "tf_elementwise: launch");
+    }
+  }
   if (VBYTES == 32 && nvec > 0 && lean && !reps_override && !persistent_env) {
     const int64_t per = 256LL * ent.unroll;
     const int64_t nblk = (nvec + per - 1) / per;
