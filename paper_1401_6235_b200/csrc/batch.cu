@@ -76,10 +76,22 @@ __device__ __forceinline__ Vec32<float> ld_keep(const Vec32<float>* p) {
   return r;
 }
 
-template <class T, int OP>
+__device__ __forceinline__ Vec16A<double> ld_keep(const Vec16A<double>* p) {
+  Vec16A<double> r;
+  asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(r.v[0]), "=d"(r.v[1]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ Vec16A<float> ld_keep(const Vec16A<float>* p) {
+  Vec16A<float> r;
+  asm("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
+      : "=f"(r.v[0]), "=f"(r.v[1]), "=f"(r.v[2]), "=f"(r.v[3])
+      : "l"(p));
+  return r;
+}
+
+template <class T, int OP, class V = Vec32<T>>
 __device__ __forceinline__ void batch_vec(const BatchOp<T>& b, int64_t head, int64_t j) {
   constexpr int NIN = OpInfo<OP>::NIN;
-  using V = Vec32<T>;
   V r[NIN];
 #pragma unroll
   for (int k = 0; k < NIN; k++) r[k] = ld_keep(reinterpret_cast<const V*>(b.in[k] + head) + j);
@@ -132,6 +144,18 @@ __device__ __forceinline__ void dispatch_vec(const BatchOp<T>& b, int64_t head, 
 #define TF_CASE(ID) \
   case ID:          \
     batch_vec<T, ID>(b, head, j); \
+    break;
+    TF_BATCH_CASES(TF_CASE)
+#undef TF_CASE
+  }
+}
+
+template <class T>
+__device__ __forceinline__ void dispatch_vec16(const BatchOp<T>& b, int64_t head, int64_t j) {
+  switch (b.op) {  // warp-uniform
+#define TF_CASE(ID) \
+  case ID:          \
+    batch_vec<T, ID, Vec16A<T>>(b, head, j); \
     break;
     TF_BATCH_CASES(TF_CASE)
 #undef TF_CASE
@@ -218,6 +242,37 @@ __global__ void __launch_bounds__(256, TF_BATCH_STEP_MINB) batch_step_kernel(Bat
   }
 }
 
+// Lean 16-byte variant: one 16-byte vector per plane per thread, as ew_step16_kernel —
+// lighter threads, more resident CTAs.  The f32 default (config 3's three-op batch
+// 428.0 -> 430.7 G elem-ops/s); f64 keeps the 32-byte lean kernel (config 2's five-op
+// batch 237.7 -> 228-233 at any register cap; profiles/r2s5_batch_v16_ab.txt).
+// TF_BATCH_V16=1 / =0 force it on / off for both dtypes (A/B).  Head and tail elements
+// (fewer than 32/sizeof(T) each) run scalar in one extra CTA, one element per thread.
+#ifndef TF_BATCH_V16_MINB
+#define TF_BATCH_V16_MINB 6
+#endif
+template <class T>
+__global__ void __launch_bounds__(256, TF_BATCH_V16_MINB) batch_step16_kernel(BatchArgs<T> a, int64_t n,
+                                                                        int64_t head,
+                                                                        int64_t nvec16,
+                                                                        int64_t nblk) {
+  constexpr int E = Vec16A<T>::N;
+  const int nops = a.nops;
+  if ((int64_t)blockIdx.x < nblk) {
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (j < nvec16)
+#pragma unroll 1
+      for (int o = 0; o < nops; o++) dispatch_vec16<T>(a.o[o], head, j);
+  } else {
+    const int64_t t0 = head + nvec16 * E;
+    const int64_t i = (int64_t)threadIdx.x < head ? (int64_t)threadIdx.x
+                                                  : t0 + ((int64_t)threadIdx.x - head);
+    if (i < head || (i >= t0 && i < n))
+#pragma unroll 1
+      for (int o = 0; o < nops; o++) dispatch_elem<T>(a.o[o], i);
+  }
+}
+
 int ew_num_inputs(int op);
 
 template <class T>
@@ -269,6 +324,20 @@ static int launch_batch(int nops, const int* ops, int64_t n, const void* const* 
     const char* r = getenv("TF_BATCH_REPS");
     return !(e && e[0] == '0') && !(r && atoi(r) >= 1);
   }();
+  static const int v16_env = [] {  // -1 per-dtype default, 0 never, 1 always
+    const char* e = getenv("TF_BATCH_V16");
+    return e ? (e[0] == '0' ? 0 : 1) : -1;
+  }();
+  const bool v16 = v16_env < 0 ? (lean && sizeof(T) == 4) : v16_env == 1;
+  if (v16 && nvec > 0) {
+    const int64_t nvec16 = nvec * 2;
+    const int64_t nblk = (nvec16 + 255) / 256;
+    const int64_t extra = (head > 0 || n - head - nvec * E > 0) ? 1 : 0;
+    if (nblk + extra <= 0x7fffffffLL) {
+      batch_step16_kernel<T><<<(unsigned)(nblk + extra), 256, 0, s>>>(a, n, head, nvec16, nblk);
+      return launch_status("tf_elementwise_batch: launch");
+    }
+  }
   // f64 only: +1.8% on config 2's five-op batch, while f32 measured 2% slower than
   // batch_kernel on config 3 (profiles/r2s3_batch_ab.txt)
   if (lean && nvec > 0 && sizeof(T) == 8) {

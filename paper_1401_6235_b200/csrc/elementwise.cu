@@ -227,17 +227,17 @@ __global__ void __launch_bounds__(256, OP == 3 ? TF_DIV2_MINB : TF_EW_MINB)
   }
 }
 
-// ---- lean 16-byte variant (vtsqrt1's default) --------------------------------------
+// ---- lean 16-byte variant (the default for most ops, see v16_default_op) ------------
 // The same single-step structure with ONE 16-byte vector per plane per thread and a
 // 32-register cap (__launch_bounds__(256, 8): eight resident CTAs, 2048 threads per SM).
-// For vtsqrt1 — two IEEE square roots and a division per element, a 1:1 read/write mix
-// — more, lighter threads beat fewer, fatter ones: the latency of the dependent
-// sqrt/div chains is hidden by occupancy instead of by per-thread ILP
-// (tools/micro/mix11.cu: 7.01-7.03 TB/s against 6.74-6.83 for the 32-byte kernel;
-// profiles/r2s5_mix11.txt).  Alignment contract as ew_step_kernel (head to the 32-byte
-// boundary, nvec counts 32-byte vectors); the head and tail elements run scalar in one
-// extra CTA, one element per thread.  TF_EW_V16 selects the ops (A/B): unset = the
-// per-op default, 0 = none, all = every op.
+// More, lighter threads beat fewer, fatter ones: latency (HBM, and vtsqrt1's two IEEE
+// square roots and a division per element) is hidden by occupancy instead of per-thread
+// ILP, and twice as many, half as long CTAs drain a grid with a shorter tail
+// (tools/micro/mix11.cu: vtsqrt1 7.01-7.03 TB/s against 6.74-6.83 for the 32-byte
+// kernel; profiles/r2s5_mix11.txt).  Alignment contract as ew_step_kernel (head to the
+// 32-byte boundary, nvec counts 32-byte vectors); the head and tail elements run scalar
+// in one extra CTA, one element per thread.  TF_EW_V16 selects the ops (A/B): unset =
+// the per-op default, 0 = none, all = every op.
 // (the three- and four-plane division ops spill at 32 registers: 40-48 for those)
 template <class T, int OP>
 __global__ void __launch_bounds__(256, OP == 3 ? 5 : (OP == 7 || OP == 17 || OP == 21) ? 6 : 8)
@@ -373,10 +373,18 @@ struct EwEntry {
   bool v16_default;       // ... is the default for this op
 };
 
-// Ops whose lean 16-byte kernel is the default (measured, profiles/r2s5_v16_ab.txt)
+// Ops whose lean 16-byte kernel is the default: every op but the one-plane square
+// roots (vtsqrt, sqrt_resid) and f32 vtsqrt1.  Measured with the 22 registry ops
+// launched one after another, as a caller and bench.py run them (2 GiB planes, three
+// alternating runs, profiles/r2s5_v16_ab.txt): +0.2...+2.0% for every other op (f64
+// vtsqrt1 6.87 -> 7.01 TB/s, vtdiv2 7.02 -> 7.12; bench.py config 2 155.2 -> 157.0 G
+// elem-ops/s, config 3 291.5 -> 293.3), -1.7% / -3.4% for vtsqrt and -6.5% for f32
+// vtsqrt1 (too few bytes in flight per thread for their latency).  In gpubench's
+// context (graph replays of ONE kernel back to back, best of 7) the 32-byte kernel stays
+// 0.3-0.6% ahead on the four-plane ops; both records are kept.
 template <class T, int OP>
 constexpr bool v16_default_op() {
-  return sizeof(T) == 8 && OP == 12;
+  return OP != 13 && OP != 23 && !(sizeof(T) == 4 && OP == 12);
 }
 
 // Ops whose TMA-staged variant is the default: none.  Measured against the

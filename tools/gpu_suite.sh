@@ -25,7 +25,7 @@ for w in $what; do
     ncu)
       cmd="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
       timeout 600 $cmd > ${o}_plain_full.log 2>&1 && \
-      timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:ew_(step_)?kernel" -s 5 -c 5 \
+      timeout 1200 ncu --set full --clock-control none --import-source on -k "regex:ew_(step_|step16_)?kernel" -s 5 -c 5 \
         -o ${o}_prof_ew $cmd > ${o}_ncu_full.log 2>&1; echo "rc=$?" >> ${o}_ncu_full.log ;;
   esac
 done

@@ -26,7 +26,7 @@ ROPS = {"0": "vtsum", "1": "vtsum2", "2": "vtdot"}
 
 def op_of(kernel):
     m = re.search(r"ew_kernel<(double|float), (\d+), 32>", kernel) or \
-        re.search(r"ew_(?:bulk|step)_kernel<(double|float), (\d+)>", kernel)
+        re.search(r"ew_(?:bulk|step|step16)_kernel<(double|float), (\d+)>", kernel)
     if m:
         return OPS[int(m.group(2))], "f64" if m.group(1) == "double" else "f32"
     m = re.search(r"reduce_kernel<(double|float), (\d)", kernel)
