@@ -50,11 +50,12 @@ def run_device(name, ins, offset=0, offsets=None):
         v = buf[offs[k]:]
         v.copy_(torch.from_numpy(np.ascontiguousarray(p)))
         planes.append(v)
-    outs = []
+    outs, bufs = [], []
     for k in range(2):
         o = offs[len(ins) + k]
-        buf = torch.full((n + o,), 7.0, dtype=dt, device=DEV)
-        outs.append(buf[o:])
+        buf = torch.full((n + o + 8,), 7.0, dtype=dt, device=DEV)  # guards either side
+        bufs.append((buf, o))
+        outs.append(buf[o:o + n])
     if name in K.RAW_OPS:
         K.raw_loop(name)(*planes, *outs)
     else:
@@ -70,6 +71,8 @@ def run_device(name, ins, offset=0, offsets=None):
         else:
             spec.func(planes[0], K.TwofoldArray(*outs))
     torch.cuda.synchronize()
+    for buf, o in bufs:  # nothing written outside the n output elements
+        assert bool((buf[:o] == 7).all()) and bool((buf[o + n:] == 7).all()), (name, offs)
     return outs[0].cpu().numpy(), outs[1].cpu().numpy()
 
 
@@ -104,6 +107,13 @@ def test_device_misaligned_views(name, fmt):
     mixed = [k % 3 for k in range(len(ins) + 2)]
     r0, r1 = run_device(name, ins, offsets=mixed)
     assert bits_equal(r0, w0) and bits_equal(r1, w1), (name, "mixed")
+    # equal modulo 16 bytes, different modulo 32 (still the all-scalar path, which
+    # streams at the vector kernels' rate: profiles/r2s5_halfaligned_probe.txt)
+    e16 = 2 if fmt == "f64" else 4
+    for lead in (0, 1):
+        half = [lead + e16 * (k % 4) for k in range(len(ins) + 2)]
+        r0, r1 = run_device(name, ins, offsets=half)
+        assert bits_equal(r0, w0) and bits_equal(r1, w1), (name, "half-aligned", lead)
 
 
 def _config1(n, seed):
