@@ -7,15 +7,21 @@
 // (NIN + 2) * sizeof(T) bytes and nothing else.
 //
 // Layout in HBM: each plane is one contiguous 1-D array (SoA, kernels.py:3-5).
-// Design: one CTA per chunk of 256*U*reps vectors (reps = 1, 2 for vtsqrt1), so
-// the hardware block scheduler balances the 148 SMs (a persistent grid left a
-// tail of idle SMs: -6..7 points of bandwidth, profiles/README.md).  Vectors are 32 bytes — sm_100's 256-bit
-// LDG/STG (LDG.E.NA.EFL2.256 / STG.E.EF.ENL2.256) — and each thread issues
-// U x NIN independent streaming loads before any math.  Planes that share a
-// common misalignment get a scalar head; the n % (32/sizeof(T)) tail is scalar
-// too — both in the same launch.  Planes with different misalignments run the
-// scalar grid-stride path (still one launch).  TF_VEC_BYTES=16 and
-// TF_EW_SCHED=persistent select the earlier variants for A/B measurements.
+// Kernels, all one launch per call and bit-identical to one another:
+//   ew_step16_kernel  the default for most ops: one CTA per 256 16-byte vectors, one
+//                     vector per plane per thread, <= 32 registers, 8 CTAs per SM
+//   ew_step_kernel    32-byte vectors (sm_100's 256-bit LDG.E.NA.EFL2.256 /
+//                     STG.E.EF.ENL2.256), one CTA per 256*U vectors; the default for
+//                     the one-plane square roots and f32 vtsqrt1
+//   ew_kernel         chunked / persistent / 16-byte A/B variants and the all-scalar
+//                     path for planes with different misalignments
+//   ew_bulk_kernel    TMA-staged inputs (cp.async.bulk ring, mbarriers), opt-in
+// Planes that share a common misalignment get a scalar head up to the 32-byte boundary;
+// the remainder below one vector is a scalar tail — both inside the same launch.  One
+// CTA per chunk lets the hardware block scheduler balance the 148 SMs (a persistent grid
+// left a tail of idle SMs: -6..7 points of bandwidth, profiles/README.md).
+// TF_EW_V16, TF_EW_LEAN, TF_VEC_BYTES=16, TF_EW_SCHED=persistent, TF_EW_REPS and
+// TF_EW_BULK select the variants for A/B measurements.
 #include <cuda_runtime.h>
 
 #include <atomic>
