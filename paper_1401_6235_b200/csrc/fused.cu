@@ -19,6 +19,8 @@
 //               out: x value/error (3 planes each)
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tf_math.cuh"
 
@@ -192,6 +194,18 @@ __global__ void __launch_bounds__(128) gauss3_kernel(const T* __restrict__ Av,
   }
 }
 
+// axpy / submul run on 16-byte vectors, the lighter-thread design that won for the
+// registry kernels (ew_step16_kernel): f64 48 registers instead of 66, 6.95 -> 7.30 TB/s
+// at 2^27 (+5%; profiles/r2s5_fused_vb_ab.txt).  TF_FUSED_VB=32 selects the 32-byte
+// vectors again (A/B).
+static bool fused_vb16() {
+  static const bool v = [] {
+    const char* e = getenv("TF_FUSED_VB");
+    return !(e && atoi(e) == 32);
+  }();
+  return v;
+}
+
 int fused_launch(int fop, int dtype, int64_t n, const void* const* in, void* const* out,
                  cudaStream_t s) {
   if (fop < 0 || fop > 3) return fail(TF_EINVAL, "tf_fused: unknown fused op id");
@@ -214,11 +228,17 @@ int fused_launch(int fop, int dtype, int64_t n, const void* const* in, void* con
   const bool f64 = dtype == TF_F64;
   switch (fop) {
     case TF_FAXPY:
-      if (f64) launch_fused_ew<double, TF_FAXPY, 32>(p, n, s);
+      if (fused_vb16()) {
+        if (f64) launch_fused_ew<double, TF_FAXPY, 16>(p, n, s);
+        else launch_fused_ew<float, TF_FAXPY, 16>(p, n, s);
+      } else if (f64) launch_fused_ew<double, TF_FAXPY, 32>(p, n, s);
       else launch_fused_ew<float, TF_FAXPY, 32>(p, n, s);
       break;
     case TF_FSUBMUL:
-      if (f64) launch_fused_ew<double, TF_FSUBMUL, 32>(p, n, s);
+      if (fused_vb16()) {
+        if (f64) launch_fused_ew<double, TF_FSUBMUL, 16>(p, n, s);
+        else launch_fused_ew<float, TF_FSUBMUL, 16>(p, n, s);
+      } else if (f64) launch_fused_ew<double, TF_FSUBMUL, 32>(p, n, s);
       else launch_fused_ew<float, TF_FSUBMUL, 32>(p, n, s);
       break;
     case TF_FQUAD:

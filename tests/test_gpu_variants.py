@@ -33,3 +33,14 @@ def test_variant_parity(env):
                        capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "mismatches: 0" in r.stdout
+
+
+@pytest.mark.gpu
+def test_fused_32_byte_variant_parity():
+    # axpy / submul default to 16-byte vectors; the 32-byte kernels (TF_FUSED_VB=32) must
+    # give the same bits: the fused parity tests again in a process with the switch set
+    e = dict(os.environ, TF_FUSED_VB="32")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(ROOT / "tests" / "test_fused.py"), "-x",
+                        "-q", "-m", "gpu", "-p", "no:cacheprovider"], env=e, capture_output=True,
+                       text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
