@@ -141,21 +141,8 @@ __global__ void __launch_bounds__(256, TF_IL_MIN_BLOCKS) ew_il_kernel(ILArgs<T> 
 #ifndef TF_IL_STEP_MIN_BLOCKS
 #define TF_IL_STEP_MIN_BLOCKS 4
 #endif
-// LIGHT: one step per thread (two for the one-plane op) under a 32-register cap (8
-// resident CTAs per SM; 48 registers for the division and square-root ops, whose
-// branch-free fast paths spill below that) —
-// the interleaved twin of ew_step16_kernel: a 32-byte pair vector is 16 bytes of each of
-// the two planes it stands for.
-template <int OP, bool LIGHT>
-constexpr int il_step_minb() {
-  return !LIGHT ? TF_IL_STEP_MIN_BLOCKS
-                : (OP == 3 || OP == 7 || OP == 11 || OP == 12 || OP == 13 || OP == 17 || OP == 21 ||
-                   OP == 22 || OP == 23)
-                      ? 5
-                      : 8;
-}
-template <class T, int OP, bool LIGHT = false>
-__global__ void __launch_bounds__(256, il_step_minb<OP, LIGHT>()) ew_il_step_kernel(ILArgs<T> p, int64_t n, int64_t nblk) {
+template <class T, int OP>
+__global__ void __launch_bounds__(256, TF_IL_STEP_MIN_BLOCKS) ew_il_step_kernel(ILArgs<T> p, int64_t n, int64_t nblk) {
   constexpr int NIN = OpInfo<OP>::NIN;
   constexpr int AR = OpInfo<OP>::ARITY;
   constexpr int E = Vec16<T>::N;
@@ -169,7 +156,7 @@ __global__ void __launch_bounds__(256, il_step_minb<OP, LIGHT>()) ew_il_step_ker
   constexpr bool XP = (AR == 22 || AR == 21 || AR == 2);
   // steps in flight per thread (all loads issue before any math); the one-plane
   // op (vtsqrt: 16 bytes in per step) carries 4 to keep enough bytes in flight
-  constexpr int U = LIGHT ? (AR == 1 ? 2 : 1) : (AR == 1 ? 4 : 2);
+  constexpr int U = AR == 1 ? 4 : 2;
   // CTA-chunked, as the split kernels: chunk = 256*U consecutive steps per CTA,
   // thread t takes steps t and t+256 (coalesced, contiguous per CTA)
   const int64_t CH = 256LL * U;
@@ -411,16 +398,7 @@ struct IlEntry {
   const void* fn;
   const void* step_fn;  // lean variant (aligned arrays)
   bool lean_default;    // the lean variant measured faster for this op
-  const void* light_fn;  // lean variant, one step per thread, <= 32 registers
-  int light_u;           // its steps per thread
-  bool light_default;
 };
-
-// Ops whose LIGHT lean kernel is the default (TF_IL_LIGHT=all / 0 force it on / off)
-template <class T, int OP>
-constexpr bool il_light_default() {
-  return false;
-}
 
 // Ops whose lean interleaved kernel is the default: f32 vtsqrt1 and vtdiv (+4.6%,
 // +2.1% at 2^27); for the rest ew_il_kernel was 0.3-1.5% faster
@@ -433,11 +411,8 @@ constexpr bool il_lean_default() {
 template <class T, int OP>
 IlEntry make_il() {
   return IlEntry{reinterpret_cast<const void*>(&ew_il_kernel<T, OP>),
-                 reinterpret_cast<const void*>(&ew_il_step_kernel<T, OP, false>),
-                 il_lean_default<T, OP>(),
-                 reinterpret_cast<const void*>(&ew_il_step_kernel<T, OP, true>),
-                 OpInfo<OP>::ARITY == 1 ? 2 : 1,
-                 il_light_default<T, OP>()};
+                 reinterpret_cast<const void*>(&ew_il_step_kernel<T, OP>),
+                 il_lean_default<T, OP>()};
 }
 template <class T, int... OPS>
 struct IlTable {
@@ -488,22 +463,6 @@ int il_launch(int op, int dtype, int64_t n, const void* a, const void* b, void* 
     return e ? (e[0] == '0' ? 0 : 1) : -1;
   }();
   const bool lean = lean_env < 0 ? ent.lean_default : lean_env == 1;
-  static const int light_env = [] {  // -1 per-op default, 0 never, 1 always
-    const char* e = getenv("TF_IL_LIGHT");
-    return e ? (e[0] == '0' ? 0 : 1) : -1;
-  }();
-  const bool light = light_env < 0 ? ent.light_default : light_env == 1;
-  if (vec && light && n >= E) {
-    const int64_t nblk = (n / E + 256LL * ent.light_u - 1) / (256LL * ent.light_u);
-    const int64_t extra = n % E ? 1 : 0;
-    if (nblk + extra <= 0x7fffffffLL) {
-      int64_t nb = nblk;
-      void* args[] = {&p, &n, &nb};
-      return cuda_status(
-          cudaLaunchKernel(ent.light_fn, dim3((unsigned)(nblk + extra)), dim3(256), args, 0, s),
-          "tf_elementwise_il: launch");
-    }
-  }
   if (vec && lean && n >= E) {
     const int64_t nblk = (n / E + 256LL * U - 1) / (256LL * U);
     const int64_t extra = n % E ? 1 : 0;

@@ -1,3 +1,4 @@
+# (Record of a removed variant: TF_IL_LIGHT no longer exists in the library.)
 # Interleaved layout: LIGHT lean kernel (TF_IL_LIGHT=all) vs the per-op defaults (TF_IL_LIGHT=0),
 # all 22 ops launched one after another (tools/ew_seq_ab.py, SEQ_LAYOUT=interleaved).
 mkdir -p gpurun_out; : > gpurun_out/il_light.jsonl
