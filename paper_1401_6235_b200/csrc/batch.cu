@@ -43,20 +43,7 @@ template <class T>
 struct BatchArgs {
   BatchOp<T> o[BMAX];
   int nops;
-  // opt-in (TF_BATCH_PREFETCH=1): distinct input planes first read by an op after
-  // the first; their vectors are prefetched into L2 at thread start, so the HBM
-  // reads of every plane of the batch are in flight from the first instruction
-  // instead of one op at a time.  Measured slower on config 2's five f64 ops
-  // (237.7 -> 222.9 G elem-ops/s: the early fetches compete with the first op's
-  // loads and the lines wait in L2 past the streaming stores) and flat on configs
-  // 1 and 3 (profiles/r2s5_batch_prefetch_ab.txt), so it is off by default.
-  int npf;
-  const T* pf[BMAX * 2];
 };
-
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
 
 // Cached read-only 32-byte load: unlike ld_stream it allocates in L1 (and keeps
 // the default L2 policy), because the batch's later ops re-read the vector.
@@ -205,16 +192,15 @@ __global__ void __launch_bounds__(256, TF_BATCH_MINB) batch_kernel(BatchArgs<T> 
 #pragma unroll 1
     for (int rr = 0; rr < reps; rr++) {
       const int64_t j = cb + (int64_t)rr * 256 + threadIdx.x;
-      if (j < nvec) {
-        for (int q = 0; q < a.npf; q++)
-          prefetch_l2(reinterpret_cast<const Vec32<T>*>(a.pf[q] + head) + j);
+      if (j < nvec)
 #pragma unroll 1
         for (int o = 0; o < nops; o++) dispatch_vec<T>(a.o[o], head, j);
-      }
     }
   }
 }
 
+// (Tried and removed, session 5: prefetch.global.L2 of the later ops' first-read planes
+// at thread start — config 2 -6%, configs 1 and 3 flat, profiles/r2s5_batch_prefetch_ab.txt.)
 // Lean variant (the f64 default when every plane shares the 32-byte alignment): one
 // CTA per 256 vectors and no loops but the ops, the scalar head and tail as masked
 // vectors in one extra CTA (thread 0 head, thread 1 tail) — the loops of
@@ -227,12 +213,9 @@ __global__ void __launch_bounds__(256, TF_BATCH_STEP_MINB) batch_step_kernel(Bat
   const int nops = a.nops;
   if ((int64_t)blockIdx.x < nblk) {
     const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    if (j < nvec) {
-      for (int q = 0; q < a.npf; q++)
-        prefetch_l2(reinterpret_cast<const Vec32<T>*>(a.pf[q] + head) + j);
+    if (j < nvec)
 #pragma unroll 1
       for (int o = 0; o < nops; o++) dispatch_vec<T>(a.o[o], head, j);
-    }
   } else if (threadIdx.x < 2) {
     const int64_t s0 = threadIdx.x == 0 ? 0 : head + nvec * E;
     const int cnt = (int)(threadIdx.x == 0 ? head : n - s0);
@@ -296,21 +279,6 @@ static int launch_batch(int nops, const int* ops, int64_t n, const void* const* 
       a.o[o].out[k] = static_cast<T*>(out[2 * o + k]);
       same = same && (reinterpret_cast<uintptr_t>(out[2 * o + k]) & amask) == mis;
     }
-  }
-  static const bool prefetch = [] {
-    const char* e = getenv("TF_BATCH_PREFETCH");
-    return e && e[0] == '1';
-  }();
-  if (prefetch) {
-    for (int o = 1; o < nops; o++)
-      for (int k = 0; k < ew_num_inputs(ops[o]); k++) {
-        const T* pl = a.o[o].in[k];
-        bool seen = false;
-        for (int o2 = 0; o2 < o && !seen; o2++)
-          for (int k2 = 0; k2 < ew_num_inputs(ops[o2]); k2++) seen = seen || a.o[o2].in[k2] == pl;
-        for (int q = 0; q < a.npf; q++) seen = seen || a.pf[q] == pl;
-        if (!seen && a.npf < BMAX * 2) a.pf[a.npf++] = pl;
-      }
   }
   const int64_t E = 32 / (int64_t)tsz;
   int64_t head = n, nvec = 0;

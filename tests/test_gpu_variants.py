@@ -1,7 +1,7 @@
 """Every selectable kernel variant is parity-checked: the A/B switches
 (TF_VEC_BYTES=16, TF_EW_SCHED=persistent, TF_EW_LEAN=0 / TF_EW_REPS — the chunked
 ew_kernel instead of the lean single-step kernel —, TF_EW_V16=all/0 — the lean 16-byte
-kernel for every op / none —, TF_BATCH_PREFETCH=1, TF_CONV_LEAN=1/0, TF_EW_BULK=0/all — the register
+kernel for every op / none —, TF_BATCH_V16=1, TF_CONV_LEAN=1/0, TF_EW_BULK=0/all — the register
 and TMA-staged elementwise paths for every op —, TF_REDUCE_PATH=bulk, the host pipeline's
 slots/chunks and its zero-copy threshold TF_HOST_ZEROCOPY_MB) are read once per
 process, so each runs tools/sanitize_smoke.py (all kernel families, odd sizes,
@@ -19,7 +19,7 @@ ROOT = Path(__file__).resolve().parents[1]
 VARIANTS = [{}, {"TF_VEC_BYTES": "16"}, {"TF_EW_SCHED": "persistent"},
             {"TF_EW_BULK": "0"}, {"TF_EW_BULK": "all"}, {"TF_EW_BULK": "all", "TF_EW_BULK_REPS": "3"},
             {"TF_EW_LEAN": "0"}, {"TF_EW_REPS": "2"}, {"TF_EW_V16": "all"}, {"TF_EW_V16": "0"},
-            {"TF_BATCH_PREFETCH": "1"}, {"TF_CONV_LEAN": "1"}, {"TF_CONV_LEAN": "0"}, {"TF_BATCH_LEAN": "0"}, {"TF_IL_LEAN": "1"},
+            {"TF_BATCH_V16": "1"}, {"TF_CONV_LEAN": "1"}, {"TF_CONV_LEAN": "0"}, {"TF_BATCH_LEAN": "0"}, {"TF_IL_LEAN": "1"},
             {"TF_REDUCE_PATH": "bulk"}, {"TF_HOST_SLOTS": "2", "TF_HOST_CHUNK_MB": "1"},
             {"TF_HOST_ZEROCOPY_MB": "0"}, {"TF_HOST_ZEROCOPY_MB": "4096"}]
 

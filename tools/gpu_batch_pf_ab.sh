@@ -1,3 +1,4 @@
+# (Record of a removed variant: TF_BATCH_PREFETCH no longer exists in the library.)
 # Device batch: L2 prefetch of the later ops' first-read planes (default) vs none
 # (TF_BATCH_PREFETCH=0).  Parity first, then alternating bench runs on one box.
 mkdir -p gpurun_out
