@@ -57,6 +57,10 @@
 #ifndef TF_U_NIN1
 #define TF_U_NIN1 2
 #endif
+// ... f64: 4 (vtsqrt 6.81 -> 6.84 TB/s; 1 loses 13%; f32 flat — profiles/r2s5_u_nin1_ab.txt)
+#ifndef TF_U_NIN1_F64
+#define TF_U_NIN1_F64 4
+#endif
 
 // shared-memory stages of the TMA-staged variant, by input-plane count (A/B builds)
 #ifndef TF_BULK_NST2
@@ -128,7 +132,7 @@ __global__ void __launch_bounds__(256, (OP == 12 && VB == 32) ? TF_SQRT_MINB
   constexpr int NIN = OpInfo<OP>::NIN;
   using V = VecN<T, VB>;
   constexpr int E = V::N;
-  constexpr int U = (VB == 32) ? (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : (NIN == 1 ? TF_U_NIN1 : 2))) : Unroll<NIN>::U;
+  constexpr int U = (VB == 32) ? (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : (NIN == 1 ? (sizeof(T) == 8 ? TF_U_NIN1_F64 : TF_U_NIN1) : 2))) : Unroll<NIN>::U;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t gstride = (int64_t)gridDim.x * blockDim.x;
   // PDL (launched with programmatic stream serialization): nothing touches
@@ -216,7 +220,7 @@ __global__ void __launch_bounds__(256, OP == 3 ? TF_DIV2_MINB : TF_EW_MINB)
     ew_step_kernel(Planes<T> p, int64_t n, int64_t head, int64_t nvec, int64_t nblk) {
   constexpr int NIN = OpInfo<OP>::NIN;
   using V = Vec32<T>;
-  constexpr int U = (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : (NIN == 1 ? TF_U_NIN1 : 2)));
+  constexpr int U = (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : (NIN == 1 ? (sizeof(T) == 8 ? TF_U_NIN1_F64 : TF_U_NIN1) : 2)));
   pdl_wait();
   pdl_trigger();
   if ((int64_t)blockIdx.x < nblk) {
@@ -411,7 +415,7 @@ constexpr bool bulk_default_op() {
 template <class T, int OP, int VB>
 EwEntry make_entry() {
   constexpr int NIN = OpInfo<OP>::NIN;
-  constexpr int U = (VB == 32) ? (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : (NIN == 1 ? TF_U_NIN1 : 2))) : Unroll<NIN>::U;
+  constexpr int U = (VB == 32) ? (OP == 12 ? TF_SQRT_U : (NIN >= 3 ? 1 : (NIN == 1 ? (sizeof(T) == 8 ? TF_U_NIN1_F64 : TF_U_NIN1) : 2))) : Unroll<NIN>::U;
   // one 256*U-vector step per CTA was fastest for every op at 2^27 (6.9-7.0 TB/s
   // for the 48 B/element ops; profiles/r1s2_chunk_reps_hbm.txt), except vtsqrt1
   // (div + 2 sqrt per element, U = 1): four steps (profiles/r2_sqrt_ab.txt)
