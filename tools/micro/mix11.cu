@@ -51,15 +51,15 @@ struct Args {
   double* out[NO];
 };
 
-template <int OP, int NI, int NO, int VB, int U, int MINB>
-__global__ void __launch_bounds__(256, MINB) k(Args<NI, NO> a, int64_t nvec) {
+template <int OP, int NI, int NO, int VB, int U, int MINB, int TPB = 256>
+__global__ void __launch_bounds__(TPB, MINB) k(Args<NI, NO> a, int64_t nvec) {
   using V = Vec<VB>;
   constexpr int E = VB / 8;
-  const int64_t base = (int64_t)blockIdx.x * (256 * U) + threadIdx.x;
+  const int64_t base = (int64_t)blockIdx.x * (TPB * U) + threadIdx.x;
   V r[U][NI];
 #pragma unroll
   for (int u = 0; u < U; u++) {
-    const int64_t j = base + u * 256;
+    const int64_t j = base + u * TPB;
     if (j < nvec) {
 #pragma unroll
       for (int q = 0; q < NI; q++) r[u][q] = ldg(reinterpret_cast<const V*>(a.in[q]) + j);
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(256, MINB) k(Args<NI, NO> a, int64_t nvec) {
   }
 #pragma unroll
   for (int u = 0; u < U; u++) {
-    const int64_t j = base + u * 256;
+    const int64_t j = base + u * TPB;
     if (j < nvec) {
       V o[NO];
 #pragma unroll
@@ -96,25 +96,25 @@ __global__ void __launch_bounds__(256, MINB) k(Args<NI, NO> a, int64_t nvec) {
 static double* buf[6];
 static int64_t N;
 
-template <int OP, int NI, int NO, int VB, int U, int MINB>
+template <int OP, int NI, int NO, int VB, int U, int MINB, int TPB = 256>
 static void run(const char* name) {
   Args<NI, NO> a;
   for (int q = 0; q < NI; q++) a.in[q] = buf[q];
   for (int q = 0; q < NO; q++) a.out[q] = buf[NI + q];
   const int64_t nvec = N / (VB / 8);
-  const int64_t blocks = (nvec + 256 * U - 1) / (256 * U);
+  const int64_t blocks = (nvec + TPB * U - 1) / (TPB * U);
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, k<OP, NI, NO, VB, U, MINB>);
+  cudaFuncGetAttributes(&fa, k<OP, NI, NO, VB, U, MINB, TPB>);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k<OP, NI, NO, VB, U, MINB>, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k<OP, NI, NO, VB, U, MINB, TPB>, TPB, 0);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int i = 0; i < 3; i++) k<OP, NI, NO, VB, U, MINB><<<(unsigned)blocks, 256>>>(a, nvec);
+  for (int i = 0; i < 3; i++) k<OP, NI, NO, VB, U, MINB, TPB><<<(unsigned)blocks, TPB>>>(a, nvec);
   std::vector<float> ts;
   for (int i = 0; i < 15; i++) {
     cudaEventRecord(e0);
-    k<OP, NI, NO, VB, U, MINB><<<(unsigned)blocks, 256>>>(a, nvec);
+    k<OP, NI, NO, VB, U, MINB, TPB><<<(unsigned)blocks, TPB>>>(a, nvec);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -143,6 +143,23 @@ int main(int argc, char** argv) {
       cudaMemcpy(buf[q] + off, h.data(), h.size() * 8, cudaMemcpyHostToDevice);
   }
   // tails plane: small relative to heads (vtsqrt1 input error plane)
+  if (argc > 2) {  // threads per CTA for the light 16-byte design (session 5)
+    for (int rep = 0; rep < 3; rep++) {
+      printf("-- threads per CTA, VB16 U1\n");
+      run<0, 4, 2, 16, 1, 8, 256>("add 4/2 tpb256 (8 CTAs)");
+      run<0, 4, 2, 16, 1, 4, 512>("add 4/2 tpb512 (4 CTAs)");
+      run<0, 4, 2, 16, 1, 16, 128>("add 4/2 tpb128 (16 CTAs)");
+      run<0, 4, 2, 16, 1, 2, 1024>("add 4/2 tpb1024 (2 CTAs)");
+      run<12, 2, 2, 16, 1, 8, 256>("vtsqrt1 tpb256 (8 CTAs)");
+      run<12, 2, 2, 16, 1, 4, 512>("vtsqrt1 tpb512 (4 CTAs)");
+      run<12, 2, 2, 16, 1, 16, 128>("vtsqrt1 tpb128 (16 CTAs)");
+      run<12, 2, 2, 16, 1, 2, 1024>("vtsqrt1 tpb1024 (2 CTAs)");
+      run<3, 4, 2, 16, 1, 5, 256>("vtdiv2 tpb256 (5 CTAs)");
+      run<3, 4, 2, 16, 1, 2, 512>("vtdiv2 tpb512 (2 CTAs)");
+      run<3, 4, 2, 16, 1, 10, 128>("vtdiv2 tpb128 (10 CTAs)");
+    }
+    return 0;
+  }
   for (int rep = 0; rep < 2; rep++) {
     printf("-- copy 1 in / 1 out (vmem)\n");
     run<0, 1, 1, 16, 1, 1>("copy 1/1 VB16 U1");
