@@ -181,6 +181,28 @@ def test_config3_f32_bit_exact_vs_oracle(oracle, name):
 
 
 @pytest.mark.parametrize("fmt", ["f64", "f32"])
+def test_head_tail_boundary_sweep_vs_oracle(oracle, fmt):
+    # every (head, tail) pair of the single-step kernels: the common misalignment sets the
+    # scalar head (0 .. 32/sizeof(T) - 1 elements), n the tail; lengths around one vector,
+    # one CTA (256 vectors of 16 or 32 bytes) and two CTAs.  Outputs are guard-banded by
+    # run_device.  vtsqrt runs the 32-byte kernel, the others the 16-byte one.
+    dtype = np.float64 if fmt == "f64" else np.float32
+    e32 = 4 if fmt == "f64" else 8
+    rng = np.random.default_rng(21)
+    lengths = sorted(set(list(range(1, 3 * e32 + 2)) +
+                         [256 * e32 // 2 + d for d in (-1, 0, 1)] +
+                         [256 * e32 + d for d in range(-e32, e32 + 1)] +
+                         [512 * e32 + d for d in (-1, 0, 1, e32 + 1)]))
+    for name, nin in (("vtadd2", 4), ("vtdiv2", 4), ("vtsqrt1", 2), ("vtsqrt", 1)):
+        for off in range(e32):
+            for n in lengths:
+                ins = [rng.uniform(0.5, 2, n).astype(dtype) for _ in range(nin)]
+                w0, w1 = oracle.elementwise(name, *ins)
+                r0, r1 = run_device(name, ins, offset=off)
+                assert bits_equal(r0, w0) and bits_equal(r1, w1), (name, fmt, off, n)
+
+
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
 def test_all_ops_random_wide_vs_oracle(oracle, fmt):
     # every op at a size with many CTAs, wide exponents, subnormal-producing tails
     from paper_1401_6235_b200 import kernels as K
