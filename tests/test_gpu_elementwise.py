@@ -554,6 +554,43 @@ def test_device_batch_all_ops_match_one_by_one(fmt, offset):
         assert bits_equal(o.error.cpu().numpy(), w.error.cpu().numpy()), name
 
 
+@pytest.mark.parametrize("fmt", ["f64", "f32"])
+def test_device_batch_head_tail_boundary_sweep(oracle, fmt):
+    # the batch kernels' head/tail CTA: every common misalignment x lengths around one
+    # vector and one CTA, three ops over shared planes, guard bands around every output
+    from paper_1401_6235_b200 import kernels as K
+
+    dt = torch.float64 if fmt == "f64" else torch.float32
+    npdt = np.float64 if fmt == "f64" else np.float32
+    e32 = 4 if fmt == "f64" else 8
+    rng = np.random.default_rng(33)
+    lengths = sorted(set(list(range(1, 2 * e32 + 2)) + [256 * e32 // 2 + d for d in (-1, 0, 1)] +
+                         [256 * e32 + d for d in (-e32, -1, 0, 1, e32)] + [512 * e32 + 3]))
+    for off in range(e32):
+        for n in lengths:
+            ins = [rng.uniform(0.5, 2, n).astype(npdt) for _ in range(4)]
+
+            def put(a):
+                buf = torch.empty(n + off, dtype=dt, device=DEV)
+                buf[off:].copy_(torch.from_numpy(a))
+                return buf[off:]
+
+            P = [put(a) for a in ins]
+            X, Y = K.TwofoldArray(P[0], P[1]), K.TwofoldArray(P[2], P[3])
+            bufs = [torch.full((n + off + 8,), 7.0, dtype=dt, device=DEV) for _ in range(6)]
+            outs = [K.TwofoldArray(bufs[2 * i][off:off + n], bufs[2 * i + 1][off:off + n])
+                    for i in range(3)]
+            K.batch([("vtadd2", X, Y, outs[0]), ("vtdiv2", X, Y, outs[1]), ("vtsqrt1", X, outs[2])])
+            torch.cuda.synchronize()
+            for b in bufs:
+                assert bool((b[:off] == 7).all()) and bool((b[off + n:] == 7).all()), (fmt, off, n)
+            for name, o, w in (("vtadd2", outs[0], oracle.elementwise("vtadd2", *ins)),
+                               ("vtdiv2", outs[1], oracle.elementwise("vtdiv2", *ins)),
+                               ("vtsqrt1", outs[2], oracle.elementwise("vtsqrt1", ins[0], ins[1]))):
+                assert bits_equal(o.value.cpu().numpy(), w[0]), (name, fmt, off, n)
+                assert bits_equal(o.error.cpu().numpy(), w[1]), (name, fmt, off, n)
+
+
 def test_device_batch_config2_step_vs_oracle(oracle):
     # the bench's config-2 step as one launch: x, y shared by add/sub/mul; the
     # divisor and sqrt planes of their own
